@@ -1,0 +1,482 @@
+"""Benchmark of the B200 hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+Primary line (BASELINE.json metric "MRG31k3p uniforms/s (HBM GB/s)"): the C5
+workload -- 2^20 MRG31k3p streams x 4096 float64 uniforms each, a 65536 x 65536
+matrix on WorkGrid(1024, 1024) (34.4 GB per step, far larger than the 126 MB
+L2), sharded over ranks by contiguous stream-ordinal blocks (strong scaling:
+the total is fixed).  `value` is uniforms/s over all ranks with states and
+output resident in HBM; `e2e` is the same metric through the public API with
+host stream states uploaded and the matrix downloaded into pinned host memory
+every step.  The line also carries the other BASELINE workloads under
+"workloads": configs[1] rnormGpu (1e9 float32 normals, 2^18 streams) and the
+fisher.sim tables/s for C3 (T4, 1e6 tables) and C4 (T10 sparse 10x10).
+
+`--impl reference` times the reference's CPU path (the oracle port of
+_kernels.py, OpenMP over all host cores; the reference is pure Python + numba,
+so there is nothing to compile into oracle/_ref) on a bounded sample of the
+same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MRG31k3p uniforms/s (HBM GB/s); fisher.sim tables/s at 1/2/4/8 B200"
+
+# C5 (BASELINE configs[4]): 2^20 streams x 4096 uniforms, grid (1024, 1024)
+C5 = dict(n_streams=1 << 20, nrow=65536, ncol=65536, g0=1024, g1=1024)
+# configs[1]: 1e9 float32 normals from 2^18 streams, grid (512, 512)
+C2 = dict(n_streams=1 << 18, nrow=31250, ncol=32000, g0=512, g1=512)
+T4 = [[5, 9, 5, 7], [9, 5, 9, 7], [8, 6, 2, 6], [10, 8, 8, 8]]
+T10_ROWS = [20000, 8000, 3000, 1000, 400, 150, 60, 25, 10, 5]
+T10_COLS = [13000, 9000, 5000, 2500, 1200, 1000, 600, 250, 75, 25]
+# FP64 ops per table at source level: F + 23E + 7S + IJ
+FOPS = {"T4": 374.0, "T10": 5955.0}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def shard(n, rank, world, align=1):
+    """contiguous block [lo, hi) of n units for `rank`, boundaries multiple of align"""
+    units = n // align
+    lo = units * rank // world * align
+    hi = units * (rank + 1) // world * align
+    return lo, hi
+
+
+class Timer:
+    """CUDA events on the launching (current) stream."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.s = torch.cuda.Event(enable_timing=True)
+        self.e = torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        self.s.record()
+
+    def stop(self):
+        self.e.record()
+        self.e.synchronize()
+        return self.s.elapsed_time(self.e)  # ms
+
+
+def barrier(torch, world):
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(torch, world, v):
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def flush_l2(torch, scratch):
+    scratch.zero_()
+
+
+# ------------------------------------------------------------------ workloads
+def run_uniform(torch, sf, rank, world, steps, warmup, cfg, kind="uniform"):
+    """C5: one fill of the full matrix per step, items sharded by columns."""
+    from paper_2201_06604_b200.grid import launch_fill
+
+    g0, g1 = cfg["g0"], cfg["g1"]
+    st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
+    lo, hi = shard(g0 * g1, rank, world, align=2 * g0)
+    cur = st.device_current()
+    dt = torch.int64 if kind == "uniform-integer" else torch.float64
+    out = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=dt, device="cuda")
+    tm = Timer(torch)
+
+    def step():
+        launch_fill(kind, cur, st.count, out, cfg["nrow"], cfg["ncol"], cfg["ncol"], g0, g1,
+                    item_lo=lo, item_hi=hi)
+
+    for _ in range(warmup):
+        step()
+    barrier(torch, world)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        tm.start()
+        for _ in range(steps):
+            step()
+        ms = tm.stop()
+        barrier(torch, world)
+    ms = max_over_ranks(torch, world, ms)
+    values = cfg["nrow"] * cfg["ncol"]
+    per_launch_ms = ms / steps
+    # algorithmic bytes of this rank's launch: its output cells + state r/w
+    my_cells = values * (hi - lo) // (g0 * g1)
+    alg_bytes = my_cells * 8 + (hi - lo) * 48 * 2
+    return dict(ms_per_step=ms / steps, value=values * steps / (ms / 1e3),
+                launch_ms=per_launch_ms, alg_bytes=alg_bytes, clocks=clk.summary(),
+                launches=steps, shard=[lo, hi])
+
+
+def run_uniform_e2e(torch, sf, rank, world, steps, cfg):
+    """Public API with host buffers: states uploaded from the host StreamSet,
+    fill_uniform(...), matrix downloaded into a pinned host array, each step."""
+    if world > 1:
+        return None  # the e2e leg is reported at N=1 (host RAM per rank)
+    g = sf.WorkGrid(cfg["g0"], cfg["g1"])
+    st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
+    req = sf.FillRequest(shape=(cfg["nrow"], cfg["ncol"]), grid=g)
+    host = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=torch.float64, pin_memory=True)
+    tm = Timer(torch)
+    buf = sf.fill_uniform(st, req)  # warm-up
+    buf.download(host)
+    del buf
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tm.start()
+    for _ in range(steps):
+        _ = st.current  # host-authoritative states: the next call uploads them
+        buf = sf.fill_uniform(st, req)
+        buf.download(host)
+        del buf
+    ms = tm.stop()
+    wall = time.perf_counter() - t0
+    values = cfg["nrow"] * cfg["ncol"]
+    return dict(value=values * steps / (ms / 1e3), unit="uniforms/s",
+                h2d_bytes_per_step=cfg["n_streams"] * 48,
+                d2h_bytes_per_step=values * 8 + cfg["n_streams"] * 48 * 0,
+                wall_s=wall, steps=steps)
+
+
+def run_normal(torch, sf, rank, world, steps, warmup, cfg, dtype):
+    from paper_2201_06604_b200.grid import launch_fill
+
+    g0, g1 = cfg["g0"], cfg["g1"]
+    st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
+    lo, hi = shard(g0 * g1, rank, world, align=g1)
+    cur = st.device_current()
+    out = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=dtype, device="cuda")
+    tm = Timer(torch)
+
+    def step():
+        launch_fill("normal", cur, st.count, out, cfg["nrow"], cfg["ncol"], cfg["ncol"], g0,
+                    g1, item_lo=lo, item_hi=hi)
+
+    for _ in range(warmup):
+        step()
+    barrier(torch, world)
+    tm.start()
+    for _ in range(steps):
+        step()
+    ms = tm.stop()
+    barrier(torch, world)
+    ms = max_over_ranks(torch, world, ms)
+    values = cfg["nrow"] * cfg["ncol"]
+    es = 4 if dtype == torch.float32 else 8
+    return dict(ms_per_step=ms / steps, value=values * steps / (ms / 1e3),
+                unit="normals/s", gbs=values * es * steps / (ms / 1e3) / 1e9, launches=steps)
+
+
+def run_fisher(torch, sf, rank, world, steps, warmup, table, n, g, scratch):
+    """One fisher_sim per step over this rank's item block + NCCL all-reduce."""
+    from paper_2201_06604_b200.fisher import launch_fisher, plan_fisher
+
+    grid = sf.WorkGrid(*g)
+    st = sf.create_streams(sf.set_base_creator(), grid.size)[0]
+    plan = plan_fisher(np.asarray(table), n, st, grid)
+    lo, hi = shard(grid.size, rank, world)
+    cur = st.device_current()
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tm = Timer(torch)
+    counts = []
+
+    def step():
+        launch_fisher(plan, cur, st.count, count, item_lo=lo, item_hi=hi)
+        if world > 1:
+            torch.distributed.all_reduce(count)
+
+    for _ in range(warmup):
+        step()
+    barrier(torch, world)
+    total_ms = 0.0
+    for _ in range(steps):
+        flush_l2(torch, scratch)
+        tm.start()
+        step()
+        total_ms += tm.stop()
+        counts.append(int(count.item()))
+    barrier(torch, world)
+    ms = max_over_ranks(torch, world, total_ms)
+    return dict(ms_per_step=ms / steps, value=plan.sim_num * steps / (ms / 1e3),
+                unit="tables/s", sim_num=plan.sim_num, counts_last=counts[-1],
+                launches=steps)
+
+
+def run_fisher_e2e(torch, sf, steps, table, n, g):
+    grid = sf.WorkGrid(*g)
+    st = sf.create_streams(sf.set_base_creator(), grid.size)[0]
+    r = sf.fisher_sim(table, n, st, grid=grid)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _ = st.current  # states live on the host between calls
+        r = sf.fisher_sim(table, n, st, grid=grid)
+    wall = time.perf_counter() - t0
+    return dict(value=r.sim_num * steps / wall, unit="tables/s",
+                h2d_bytes_per_step=grid.size * 48 + 8 * (sum(map(sum, table)) + 1),
+                d2h_bytes_per_step=8 + grid.size * 48)
+
+
+# --------------------------------------------------------------- CPU baselines
+def cpu_uniform_sample(orc, rows, threads=0):
+    """C5 rows [0, rows) -- every item, rows/g0 owned rows each -- on the oracle."""
+    c = C5
+    states, _ = orc.create_streams((12345,) * 6, c["n_streams"])
+    out = np.empty((rows, c["ncol"]), np.float64)
+    t0 = time.perf_counter()
+    orc.fill_real(states, out.ravel(), rows, c["ncol"], c["ncol"], c["g0"], c["g1"], 0, 1.0,
+                  threads)
+    dt = time.perf_counter() - t0
+    return rows * c["ncol"] / dt, dt
+
+
+def cpu_baseline(reps=3, rows=2048):
+    from oracle import oracle as orc
+
+    orc.lib()
+    cpu_uniform_sample(orc, 64)  # warm
+    best = max(cpu_uniform_sample(orc, rows)[0] for _ in range(reps))
+    return {"value": best, "unit": "uniforms/s", "cores": orc.max_threads(), "kind": "port",
+            "sample": f"C5 rows [0,{rows}) = {rows * C5['ncol']} float64 uniforms from all "
+                      f"2^20 streams (oracle C port of _kernels.fill_real, OpenMP), best of {reps}"}
+
+
+def cpu_fisher(table, n_items, reps, g=(256, 64)):
+    from oracle import oracle as orc
+    from scipy.special import gammaln
+
+    t = np.asarray(table)
+    lf = gammaln(np.arange(t.sum() + 1, dtype=np.float64) + 1.0)
+    thr = float(-gammaln(t + 1.0).sum())
+    states, _ = orc.create_streams((12345,) * 6, g[0] * g[1])
+    t0 = time.perf_counter()
+    orc.fisher_replicates(states, t.sum(1), t.sum(0), lf, thr + 1e-7 * abs(thr), reps, n_items)
+    dt = time.perf_counter() - t0
+    return n_items * reps / dt
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+
+    orc.lib()
+    rows = 2048
+    cpu_uniform_sample(orc, 64)
+    for _ in range(args.warmup):
+        cpu_uniform_sample(orc, rows)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_uniform_sample(orc, rows)[1])
+    total = time.perf_counter() - t0
+    n = rows * C5["ncol"]
+    v = n * args.steps / sum(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "uniforms/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 runifGpu (bounded CPU sample: rows [0,2048) of the "
+                                   "65536x65536 matrix on WorkGrid(1024,1024))",
+                       "streams": C5["n_streams"]},
+            "cpu_baseline": {"value": v, "unit": "uniforms/s", "cores": orc.max_threads(),
+                             "kind": "port",
+                             "sample": f"{n} uniforms per step, oracle C port of "
+                                       "_kernels.fill_real (OpenMP, all host cores)"},
+            "e2e": {"value": v, "unit": "uniforms/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    try:
+        line["workloads"] = {
+            "fisher_T4_tables_per_s": cpu_fisher(T4, 16384, 4),
+            "fisher_T10_tables_per_s": cpu_fisher(np.array(_t10()), 16384, 1),
+        }
+    except Exception as e:  # noqa: BLE001
+        line["workloads"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+
+
+def _t10():
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
+        return json.load(fh)["T10"]
+
+
+# ---------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--only", default=None, help="primary|normal|fisher (debug)")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2201_06604_b200 as sf
+    from paper_2201_06604_b200 import _lib
+
+    _lib.require_device()
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2, for flushes
+    peak, peak_kind = peaks()
+
+    prim = run_uniform(torch, sf, rank, world, args.steps, args.warmup, C5)
+    workloads = {}
+    if args.only in (None, "normal"):
+        n32 = run_normal(torch, sf, rank, world, args.steps, args.warmup, C2, torch.float32)
+        workloads["rnormGpu_f32_1e9"] = {k: n32[k] for k in ("value", "unit", "ms_per_step",
+                                                              "gbs")}
+        workloads["rnormGpu_f32_1e9"]["config"] = "configs[1]: 1e9 float32 normals, 2^18 " \
+                                                  "streams, shape (31250,32000), grid (512,512)"
+    if args.only in (None, "fisher"):
+        f4 = run_fisher(torch, sf, rank, world, max(3, args.steps // 2), args.warmup, T4,
+                        10 ** 6, (256, 64), scratch)
+        workloads["fisher_T4_1e6"] = dict(value=f4["value"], unit="tables/s",
+                                          ms_per_step=f4["ms_per_step"],
+                                          counts=f4["counts_last"], sim_num=f4["sim_num"],
+                                          fp64_ops_per_table=FOPS["T4"],
+                                          config="configs[2]/C3: T4, 1e6 -> 1015808 tables, "
+                                                 "grid (256,64)")
+        t10 = np.array(_t10())
+        # C4 per-GPU share: 2^21 items on grid (2048,1024); reps bounded for the
+        # default run (1e10 tables would take ~a minute per GPU)
+        n10 = (1 << 21) * 8 * world
+        f10 = run_fisher(torch, sf, rank, world, 3, 1, t10, n10, (2048, 1024), scratch)
+        workloads["fisher_T10"] = dict(value=f10["value"], unit="tables/s",
+                                       ms_per_step=f10["ms_per_step"], sim_num=f10["sim_num"],
+                                       fp64_ops_per_table=FOPS["T10"],
+                                       config=f"configs[3]/C4 shape: T10 sparse 10x10 on grid "
+                                              f"(2048,1024), {f10['sim_num']} tables per step")
+    e2e = run_uniform_e2e(torch, sf, rank, world, min(args.steps, 3), C5)
+    if args.only in (None, "fisher") and world == 1:
+        fe = run_fisher_e2e(torch, sf, 3, T4, 10 ** 6, (256, 64))
+        workloads["fisher_T4_1e6"]["e2e"] = fe
+
+    if rank != 0:
+        return
+    achieved = prim["alg_bytes"] / (prim["launch_ms"] / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": prim["value"], "unit": "uniforms/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": prim["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "C5 runifGpu: 2^20 MRG31k3p streams x 4096 float64 uniforms "
+                               "(65536x65536 on WorkGrid(1024,1024)), one fill per step",
+                   "streams": C5["n_streams"], "uniforms_per_step": C5["nrow"] * C5["ncol"],
+                   "l2": "output 34.4 GB per step >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"stream-ordinal blocks x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "kernel": "fill_uniform_fast<0>",
+                     "algorithmic_bytes_per_launch": prim["alg_bytes"]},
+        "clocks": prim["clocks"],
+        "gpu_launches": prim["launches"],
+        "workloads": workloads,
+    }
+    if e2e:
+        line["e2e"] = {k: e2e[k] for k in ("value", "unit", "h2d_bytes_per_step",
+                                           "d2h_bytes_per_step")}
+    if not args.no_cpu and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline()
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * sfb.h -- C ABI of the B200-native streamforge hot path (libsfb.so).
+ *
+ * This is the drop-in seam that replaces the reference's Python->numba
+ * boundary, the `_kernels` module (/root/reference/pkg/src/streamforge/
+ * _kernels.py), plus the exact-integer stream arithmetic of core.py.  Every
+ * entry point names the reference interface it replaces (file:line, paths
+ * relative to /root/reference/pkg/src/streamforge/).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / C++ types cross the ABI;
+ *   - every function returns 0 (SFB_OK) or a negative SFB_E_* code, with a
+ *     thread-local message in sfb_last_error(); codes map 1:1 onto the
+ *     reference exception classes (errors.py:8-32) or CUDA failures;
+ *   - no C++ exception ever crosses the ABI;
+ *   - "device" functions take device pointers and a cudaStream_t passed as
+ *     void*; they are stream-ordered and return after enqueueing (the Python
+ *     layer synchronises where the reference is synchronous);
+ *   - stream states use the reference layout: int64 (n, 6) C-contiguous,
+ *     row w = (g1[0..2], g2[0..2]) newest-first (core.py:161-172), mutated in
+ *     place exactly where the reference kernels mutate `cur`.
+ */
+#ifndef SFB_H_
+#define SFB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFB_OK 0
+#define SFB_E_INVALID_ARGUMENT (-1)      /* errors.py:12 InvalidArgumentError */
+#define SFB_E_INSUFFICIENT_STREAMS (-2)  /* errors.py:20 InsufficientStreamsError */
+#define SFB_E_INVALID_GRID (-3)          /* errors.py:24 InvalidGridError */
+#define SFB_E_INVALID_RATE (-4)          /* errors.py:28 InvalidRateError */
+#define SFB_E_INVALID_MARGINS (-5)       /* errors.py:32 InvalidMarginsError */
+#define SFB_E_INVALID_SEED (-6)          /* errors.py:8 InvalidSeedError */
+#define SFB_E_CORRUPT_STREAM_FILE (-7)   /* errors.py:16 CorruptStreamFileError */
+#define SFB_E_IO (-8)                    /* OSError from open()/write() */
+#define SFB_E_CUDA (-100)                /* CUDA runtime / launch failure */
+
+/* output element types */
+#define SFB_F64 0
+#define SFB_F32 1
+#define SFB_I64 2
+
+/* ---- library ----------------------------------------------------------- */
+const char *sfb_last_error(void);
+int sfb_version(void);
+/* 1 when the library was built for sm_100a and a device is visible */
+int sfb_device_ok(void);
+
+/* ---- host stream arithmetic (exact integers; core.py) -------------------- */
+/* core.py:79-86 validate_seed -> SFB_E_INVALID_SEED */
+int sfb_validate_seed(const int64_t seed[6]);
+/* core.py:114-123 next_state: one step, z in [1, m1] */
+int sfb_next_state(int64_t state[6], int64_t *z);
+/* core.py:55-62 _jump_matrices(e): T1^(2^e) mod m1, T2^(2^e) mod m2 (row-major) */
+int sfb_jump_matrices(int e, int64_t j1[9], int64_t j2[9]);
+/* core.py:126-136 jump_ahead(s, e): advance 2^e steps */
+int sfb_jump_ahead(int64_t state[6], int e);
+/* generalisation used by the chunked kernels: advance n steps (any n) */
+int sfb_skip(int64_t state[6], uint64_t n);
+/* core.py:222-235 create_streams + core.py:139-142 _jump_seed:
+ * rows[k] = J^k seed (J = T^(2^134)); next_seed = J^n seed. */
+int sfb_create_streams(const int64_t seed[6], int64_t n, int64_t *rows,
+                       int64_t next_seed[6]);
+
+/* ---- stream files (core.py:238-305) ------------------------------------ */
+/* bytes needed by sfb_format_streams (upper bound) */
+int64_t sfb_format_streams_bound(int64_t n);
+/* core.py:242-250 save_streams: writes the exact text into buf; *len = bytes */
+int sfb_format_streams(const int64_t *current, const int64_t *initial, int64_t n,
+                       char *buf, int64_t cap, int64_t *len);
+/* core.py:238-261 save_streams / save_streams_atomic to a path
+ * (atomic: temp file + fsync + rename, core.py:253-261) */
+int sfb_save_streams(const char *path, const int64_t *current,
+                     const int64_t *initial, int64_t n, int atomic);
+/* core.py:264-305 load_streams, split in two: count from the header, then
+ * the parse (same checks, same error class: SFB_E_CORRUPT_STREAM_FILE). */
+int sfb_parse_streams_count(const char *text, int64_t len, int64_t *n);
+int sfb_parse_streams(const char *text, int64_t len, int64_t *current,
+                      int64_t *initial, int64_t n);
+
+/* ---- device fills (grid.py:112-144 run_grid -> _kernels) --------------- */
+/* _kernels.py:50-80 fill_real: mode 0 uniform (f64 out), mode 1 exponential
+ * (f64 out, rate > 0).  Work item w=(i,j) = i + g0*j owns cells
+ * {r = i mod g0, c = j mod g1}, row-major.  Only items with ordinal in
+ * [item_lo, item_hi) run (multi-GPU shard; the whole grid is [0, g0*g1)).
+ * Padding columns [ncol, npad) of every row are zeroed when zero_pad != 0.
+ * d_cur: device int64 (n_streams, 6); d_out: device f64 (nrow, npad). */
+int sfb_fill_real(int64_t *d_cur, int64_t n_streams, double *d_out, int64_t nrow,
+                  int64_t ncol, int64_t npad, int64_t g0, int64_t g1, int mode,
+                  double rate, int64_t item_lo, int64_t item_hi, int zero_pad,
+                  void *stream);
+/* _kernels.py:83-105 fill_integer: raw z in [1, m1] into int64 */
+int sfb_fill_integer(int64_t *d_cur, int64_t n_streams, int64_t *d_out,
+                     int64_t nrow, int64_t ncol, int64_t npad, int64_t g0,
+                     int64_t g1, int64_t item_lo, int64_t item_hi, int zero_pad,
+                     void *stream);
+/* _kernels.py:108-166 fill_normal: paired-lane Box-Muller, row-major stream
+ * ordinal s = i*g1 + j (pairs j even).  out_dtype SFB_F64 or SFB_F32 (the
+ * float32 extension rounds the fp64 result once).  Shard range [item_lo,
+ * item_hi) is in stream ordinals and must be pair aligned.  g1 must be even
+ * (SFB_E_INVALID_GRID, grid.py:37-40). */
+int sfb_fill_normal(int64_t *d_cur, int64_t n_streams, void *d_out, int out_dtype,
+                    int64_t nrow, int64_t ncol, int64_t npad, int64_t g0,
+                    int64_t g1, int64_t item_lo, int64_t item_hi, int zero_pad,
+                    void *stream);
+
+/* ---- device Fisher simulation (fisher.py:118-164 -> _kernels) ----------- */
+/* _kernels.py:169-286 fisher_replicates over items [item_lo, item_hi):
+ * each item runs `reps` replicates on its own stream; the hit count
+ * (stat <= threshold) is ADDED to *d_count (device uint64; zero it first, or
+ * pass zero_count=1).  d_stats (nullable, device f64) receives the statistic of
+ * replicate rep of item w at (w - item_lo)*reps + rep (work-item major,
+ * _kernels.py:277-278).  d_item_counts (nullable, device int64) receives the
+ * per-item hit counts.  nrowt/ncolt/lf are HOST arrays (the margins and the
+ * scipy gammaln table, fisher.py:70-72); lf_len = total + 1. */
+int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrowt,
+                          int nr, const int64_t *ncolt, int nc, const double *lf,
+                          int64_t lf_len, double threshold, int64_t reps,
+                          int64_t item_lo, int64_t item_hi, double *d_stats,
+                          int64_t *d_item_counts, uint64_t *d_count,
+                          int zero_count, void *stream);
+/* _kernels.py:289-391 rcont2_table: one table from one 6-word state, run by
+ * the same device sampler on one thread.  d_state: device int64[6] (mutated),
+ * d_mat: device int64[nr*nc]. */
+int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
+                     const double *lf, int64_t lf_len, int64_t *d_state,
+                     int64_t *d_mat, void *stream);
+
+/* ---- test hooks (host execution of the device arithmetic) --------------- */
+/* runs the uint32 device step formulation on the host: n states x steps,
+ * writes the outputs z and advances states (int64 (n,6)) */
+int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out);
+/* the device exp() port (glibc __exp FMA variant) evaluated on the host */
+double sfb_host_exp(double x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFB_H_ */

@@ -1,0 +1,118 @@
+"""ctypes binding of libsfb.so (include/sfb.h) -- the only way into the kernels.
+
+There is deliberately no fallback: if the shared library is missing or was not
+built for sm_100a, every device entry point raises.  (The reference's own CPU
+path lives only in oracle/, which this package never imports.)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsfb.so")
+
+SFB_F64, SFB_F32, SFB_I64 = 0, 1, 2
+
+_ERRORS = {
+    -1: errors.InvalidArgumentError,
+    -2: errors.InsufficientStreamsError,
+    -3: errors.InvalidGridError,
+    -4: errors.InvalidRateError,
+    -5: errors.InvalidMarginsError,
+    -6: errors.InvalidSeedError,
+    -7: errors.CorruptStreamFileError,
+    -8: OSError,
+    -100: errors.DeviceError,
+}
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+
+_SIGS = {
+    "sfb_last_error": ([], ctypes.c_char_p),
+    "sfb_version": ([], _int),
+    "sfb_device_ok": ([], _int),
+    "sfb_validate_seed": ([_i64p], _int),
+    "sfb_next_state": ([_i64p, _i64p], _int),
+    "sfb_jump_matrices": ([_int, _i64p, _i64p], _int),
+    "sfb_jump_ahead": ([_i64p, _int], _int),
+    "sfb_skip": ([_i64p, ctypes.c_uint64], _int),
+    "sfb_create_streams": ([_i64p, _i64, _i64p, _i64p], _int),
+    "sfb_format_streams_bound": ([_i64], _i64),
+    "sfb_format_streams": ([_i64p, _i64p, _i64, ctypes.c_char_p, _i64, _i64p], _int),
+    "sfb_save_streams": ([ctypes.c_char_p, _i64p, _i64p, _i64, _int], _int),
+    "sfb_parse_streams_count": ([ctypes.c_char_p, _i64, _i64p], _int),
+    "sfb_parse_streams": ([ctypes.c_char_p, _i64, _i64p, _i64p, _i64], _int),
+    "sfb_fill_real": ([_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _int, ctypes.c_double,
+                       _i64, _i64, _int, _vp], _int),
+    "sfb_fill_integer": ([_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int, _vp],
+                         _int),
+    "sfb_fill_normal": ([_vp, _i64, _vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int,
+                         _vp], _int),
+    "sfb_fisher_replicates": ([_vp, _i64, _i64p, _int, _i64p, _int, _f64p, _i64,
+                               ctypes.c_double, _i64, _i64, _i64, _vp, _vp, _vp, _int, _vp],
+                              _int),
+    "sfb_rcont2_table": ([_i64p, _int, _i64p, _int, _f64p, _i64, _vp, _vp, _vp], _int),
+    "sfb_host_step_u32": ([_i64p, _i64, _i64, _i64p], _int),
+    "sfb_host_exp": ([ctypes.c_double], ctypes.c_double),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """Load libsfb.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = lib().sfb_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, errors.DeviceError)(msg)
+
+
+def ptr(a, t=_i64p):
+    """ctypes pointer to a numpy array's buffer."""
+    return a.ctypes.data_as(t)
+
+
+def dptr(t) -> int:
+    """raw device address of a torch tensor."""
+    return t.data_ptr()
+
+
+def require_device():
+    """The product path needs an sm_100a GPU; fail loudly otherwise."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise errors.DeviceError("no CUDA device visible: the B200 kernels have no CPU fallback")
+    if not lib().sfb_device_ok():
+        raise errors.DeviceError("libsfb.so is built for sm_100a only (B200); this device is not")
+
+
+def stream_handle():
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream

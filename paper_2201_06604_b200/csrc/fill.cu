@@ -1,0 +1,453 @@
+// fill.cu -- sm_100a generation kernels: uniform / integer / exponential and
+// paired-lane Box-Muller fills (the reference's _kernels.fill_real,
+// fill_integer, fill_normal: _kernels.py:50-166, dispatched by grid.run_grid,
+// grid.py:112-144).
+//
+// Layout contract (grid.py:73-102): work item (i, j) of the g0 x g1 grid owns
+// the cells {(r, c): r = i mod g0, c = j mod g1} and visits them row-major,
+// one MRG31k3p step per cell (uniform kinds) or one step of each of the two
+// lane streams per cell pair (normal).  Stream ordinals: i + g0*j for the
+// uniform kinds, i*g1 + j for normals.  Unused streams are never touched and
+// padding columns are never written by the kernels (they are zeroed by a
+// cudaMemset2DAsync when requested, matching MatrixBuffer's np.zeros).
+//
+// B200 decomposition: since every cell consumes exactly one
+// step, the state at any draw index d of an item is A^d s_item, so the work of
+// one item is split into chunks whose start states are reached by jump-ahead
+// (powers A^(2^b) passed by value as kernel parameters).  Results are
+// bit-identical for every chunking, exactly like the reference's thread-count
+// invariance (tests/test_grid.py:91-103).
+//
+//  * *_fast kernels: the dominant layouts (g1 even, npad even): one thread
+//    drives the two streams of a column pair (j, j+1) over a block of owned
+//    rows and writes both values with one 16-byte (f64/i64) or 8-byte (f32)
+//    streaming store; adjacent lanes own adjacent pairs, so a warp writes 512
+//    contiguous bytes per step (coalesced, HBM-write bound).
+//  * *_generic kernels: any grid / shape / shard (odd g1, vectors, ragged
+//    shards): one thread per (item, chunk of draws), scalar stores.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "sfb_internal.h"
+
+namespace sfb {
+
+constexpr double kTwoPiNorm = (2.0 * 3.141592653589793) / 2147483648.0;  // TWOPI*NORM, exact
+constexpr double kHalfPi = 0.5 * 3.141592653589793;                      // _kernels.py:22
+
+enum Kind { kUniform = 0, kExponential = 1, kInteger = 2 };
+
+struct Geom {
+    int64_t nrow, ncol, npad, g0, g1;
+};
+
+// number of owned rows of grid row i / owned columns of grid column j
+__device__ __forceinline__ int64_t owned(int64_t n, int64_t idx, int64_t g) {
+    return idx < n ? (n - idx + g - 1) / g : 0;
+}
+
+template <int KIND>
+__device__ __forceinline__ double real_value(uint32_t z, double rate) {
+    const double u = (double)z * kNorm;  // _kernels.py:70, exact
+    if (KIND == kUniform) return u;
+    return -log1p(-u) / rate;  // _kernels.py:74 (CUDA log1p: tolerance, not bit-exact)
+}
+
+// ---------------------------------------------------------------------------
+// uniform kinds, generic layout
+template <int KIND>
+__global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict__ cur,
+                                                            void *__restrict__ out, Geom g,
+                                                            int64_t item_lo, int64_t nloc,
+                                                            int64_t chunk, int64_t nunits,
+                                                            double rate, const __grid_constant__ Pow2Table tab) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= nunits) return;
+    const int64_t w = item_lo + u % nloc;
+    const int64_t c = u / nloc;
+    const int64_t i = w % g.g0, j = w / g.g0;
+    const int64_t nr = owned(g.nrow, i, g.g0), nc = owned(g.ncol, j, g.g1);
+    const int64_t total = nr * nc;
+    const int64_t d0 = c * chunk;
+    if (d0 >= total) return;
+    const int64_t d1 = min(d0 + chunk, total);
+    Mrg s = load_state(cur + 6 * w);
+    skip(tab, s, (uint64_t)d0);
+    int64_t rho = d0 / nc, q = d0 % nc;
+    for (int64_t d = d0; d < d1; ++d) {
+        const uint32_t z = step(s);
+        const int64_t off = (i + g.g0 * rho) * g.npad + j + g.g1 * q;
+        if (KIND == kInteger)
+            __stcs((long long *)out + off, (long long)z);
+        else
+            __stcs((double *)out + off, real_value<KIND>(z, rate));
+        if (++q == nc) {
+            q = 0;
+            ++rho;
+        }
+    }
+    if (d1 == total) store_state(cur + 6 * w, s);
+}
+
+// uniform kinds, column-pair fast path (g1 even, npad even, shard = whole pairs)
+// unit = (chunk c, grid row i, pair jp): adjacent lanes = adjacent pairs
+template <int KIND>
+__global__ void __launch_bounds__(256) fill_uniform_fast(int64_t *__restrict__ cur,
+                                                         void *__restrict__ out, Geom g,
+                                                         int64_t j_lo, int64_t npairs,
+                                                         int64_t rows_per_chunk, int64_t nunits,
+                                                         double rate, const __grid_constant__ Pow2Table tab) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= nunits) return;
+    const int64_t jp = u % npairs;
+    const int64_t ic = u / npairs;
+    const int64_t i = ic % g.g0, c = ic / g.g0;
+    const int64_t j = j_lo + 2 * jp;
+    const int64_t nr = owned(g.nrow, i, g.g0);
+    const int64_t rho0 = c * rows_per_chunk;
+    if (rho0 >= nr) return;
+    const int64_t rho1 = min(rho0 + rows_per_chunk, nr);
+    const int64_t na = owned(g.ncol, j, g.g1), nb = owned(g.ncol, j + 1, g.g1);
+    const int64_t wa = i + g.g0 * j, wb = wa + g.g0;
+    Mrg sa = load_state(cur + 6 * wa), sb = load_state(cur + 6 * wb);
+    if (rho0) {
+        skip(tab, sa, (uint64_t)(rho0 * na));
+        skip(tab, sb, (uint64_t)(rho0 * nb));
+    }
+    for (int64_t rho = rho0; rho < rho1; ++rho) {
+        const int64_t rowoff = (i + g.g0 * rho) * g.npad + j;
+        if (KIND == kInteger) {
+            longlong2 *p = (longlong2 *)((long long *)out + rowoff);
+            const int64_t stride = g.g1 / 2;
+#pragma unroll 3
+            for (int64_t q = 0; q < nb; ++q) {
+                longlong2 v;
+                v.x = step(sa);
+                v.y = step(sb);
+                __stcs(p + q * stride, v);
+            }
+            if (na > nb) __stcs((long long *)out + rowoff + g.g1 * nb, (long long)step(sa));
+        } else {
+            double2 *p = (double2 *)((double *)out + rowoff);
+            const int64_t stride = g.g1 / 2;
+#pragma unroll 3
+            for (int64_t q = 0; q < nb; ++q) {
+                double2 v;
+                v.x = real_value<KIND>(step(sa), rate);
+                v.y = real_value<KIND>(step(sb), rate);
+                __stcs(p + q * stride, v);
+            }
+            if (na > nb)
+                __stcs((double *)out + rowoff + g.g1 * nb, real_value<KIND>(step(sa), rate));
+        }
+    }
+    if (rho1 == nr) {
+        store_state(cur + 6 * wa, sa);
+        store_state(cur + 6 * wb, sb);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Box-Muller pair (_kernels.py:145-152), computed in fp64:
+//   u1 = z1*NORM, theta = (2 pi NORM)*z2, R = sqrt(-2 log u1),
+//   a = R cos(theta), b = R cos(theta - pi/2)
+// CUDA's log/cos are within 1-2 ulp of glibc's (tolerance stated in
+// DESIGN.md and tests); the float32 variant rounds the fp64 value once.
+__device__ __forceinline__ void box_muller(uint32_t z1, uint32_t z2, double &a, double &b) {
+    const double u1 = (double)z1 * kNorm;
+    const double theta = kTwoPiNorm * (double)z2;
+    const double radius = sqrt(-2.0 * log(u1));
+    a = radius * cos(theta);
+    b = radius * cos(theta - kHalfPi);
+}
+
+template <typename T>
+__device__ __forceinline__ void put(T *out, int64_t off, double v) {
+    __stcs(out + off, (T)v);
+}
+
+// normal, generic layout: unit = (pair, chunk of pair-iterations)
+template <typename T>
+__global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__ cur,
+                                                           T *__restrict__ out, Geom g,
+                                                           int64_t pair_lo, int64_t nloc,
+                                                           int64_t chunk, int64_t nunits,
+                                                           const __grid_constant__ Pow2Table tab) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= nunits) return;
+    const int64_t p = pair_lo + u % nloc;
+    const int64_t c = u / nloc;
+    const int64_t half = g.g1 / 2;
+    const int64_t i = p / half, j0 = 2 * (p % half);  // _kernels.py:125-128
+    const int64_t s0 = i * g.g1 + j0;
+    const int64_t nr = owned(g.nrow, i, g.g0);
+    const int64_t niter = owned(g.ncol, j0, g.g1);  // `while ca < ncol` trips per row
+    const int64_t total = nr * niter;
+    const int64_t d0 = c * chunk;
+    if (d0 >= total) return;
+    const int64_t d1 = min(d0 + chunk, total);
+    Mrg sa = load_state(cur + 6 * s0), sb = load_state(cur + 6 * (s0 + 1));
+    skip(tab, sa, (uint64_t)d0);
+    skip(tab, sb, (uint64_t)d0);
+    int64_t rho = d0 / niter, q = d0 % niter;
+    for (int64_t d = d0; d < d1; ++d) {
+        const uint32_t z1 = step(sa), z2 = step(sb);
+        double a, b;
+        box_muller(z1, z2, a, b);
+        const int64_t ca = j0 + g.g1 * q;
+        const int64_t off = (i + g.g0 * rho) * g.npad + ca;
+        put(out, off, a);
+        if (ca + 1 < g.ncol) put(out, off + 1, b);  // partner discarded past ncol
+        if (++q == niter) {
+            q = 0;
+            ++rho;
+        }
+    }
+    if (d1 == total) {
+        store_state(cur + 6 * s0, sa);
+        store_state(cur + 6 * (s0 + 1), sb);
+    }
+}
+
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+    using type = double2;
+};
+template <>
+struct Vec2<float> {
+    using type = float2;
+};
+
+// normal, pair fast path (npad even): unit = (chunk, grid row i, pair jp)
+template <typename T>
+__global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cur,
+                                                        T *__restrict__ out, Geom g,
+                                                        int64_t i_lo, int64_t nrows_grid,
+                                                        int64_t rows_per_chunk, int64_t nunits,
+                                                        const __grid_constant__ Pow2Table tab) {
+    using V = typename Vec2<T>::type;
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= nunits) return;
+    const int64_t half = g.g1 / 2;
+    const int64_t jp = u % half;
+    const int64_t ic = u / half;
+    const int64_t i = i_lo + ic % nrows_grid, c = ic / nrows_grid;
+    const int64_t j0 = 2 * jp;
+    const int64_t nr = owned(g.nrow, i, g.g0);
+    const int64_t rho0 = c * rows_per_chunk;
+    if (rho0 >= nr) return;
+    const int64_t rho1 = min(rho0 + rows_per_chunk, nr);
+    const int64_t niter = owned(g.ncol, j0, g.g1);
+    const int64_t s0 = i * g.g1 + j0;
+    Mrg sa = load_state(cur + 6 * s0), sb = load_state(cur + 6 * (s0 + 1));
+    if (rho0) {
+        skip(tab, sa, (uint64_t)(rho0 * niter));
+        skip(tab, sb, (uint64_t)(rho0 * niter));
+    }
+    // the last trip of a row may have its partner column past ncol
+    const bool partner_last = j0 + 1 + g.g1 * (niter - 1) < g.ncol;
+    const int64_t nfull = partner_last ? niter : niter - 1;
+    for (int64_t rho = rho0; rho < rho1; ++rho) {
+        const int64_t rowoff = (i + g.g0 * rho) * g.npad + j0;
+        V *p = (V *)(out + rowoff);
+#pragma unroll 3
+        for (int64_t q = 0; q < nfull; ++q) {
+            double a, b;
+            box_muller(step(sa), step(sb), a, b);
+            V v;
+            v.x = (T)a;
+            v.y = (T)b;
+            __stcs(p + q * half, v);
+        }
+        if (nfull < niter) {
+            double a, b;
+            box_muller(step(sa), step(sb), a, b);
+            put(out, rowoff + g.g1 * nfull, a);
+        }
+    }
+    if (rho1 == nr) {
+        store_state(cur + 6 * s0, sa);
+        store_state(cur + 6 * (s0 + 1), sb);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch planning
+
+constexpr int kThreads = 256;
+// enough units to fill 148 SMs several times over (2048 resident threads/SM)
+constexpr int64_t kTargetUnits = 148LL * 2048 * 3;
+constexpr int64_t kMinChunkDraws = 512;
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static int launch_check(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+static int check_common(int64_t n_streams, int64_t nrow, int64_t ncol, int64_t npad, int64_t g0,
+                        int64_t g1, int64_t item_lo, int64_t item_hi) {
+    if (g0 < 1 || g1 < 1) return fail(SFB_E_INVALID_GRID, "work grid dimensions must be >= 1");
+    if (nrow < 1 || ncol < 1) return fail(SFB_E_INVALID_ARGUMENT, "matrix dimensions must be >= 1");
+    if (npad < ncol) return fail(SFB_E_INVALID_ARGUMENT, "npad must be >= ncol");
+    if (n_streams < g0 * g1)
+        return fail(SFB_E_INSUFFICIENT_STREAMS, "grid needs %lld streams, got %lld",
+                    (long long)(g0 * g1), (long long)n_streams);
+    if (item_lo < 0 || item_hi > g0 * g1 || item_lo > item_hi)
+        return fail(SFB_E_INVALID_ARGUMENT, "item range [%lld, %lld) outside the grid",
+                    (long long)item_lo, (long long)item_hi);
+    return SFB_OK;
+}
+
+static int zero_padding(void *out, size_t elsize, int64_t nrow, int64_t ncol, int64_t npad,
+                        cudaStream_t st) {
+    if (npad == ncol) return SFB_OK;
+    cudaError_t e = cudaMemset2DAsync((char *)out + ncol * elsize, npad * elsize, 0,
+                                      (npad - ncol) * elsize, nrow, st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "padding memset: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+template <int KIND>
+static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_lo,
+                          int64_t item_hi, double rate, cudaStream_t st) {
+    Pow2Table tab;
+    pow2_table(&tab);
+    const int64_t nloc = item_hi - item_lo;
+    if (nloc == 0) return SFB_OK;
+    const int64_t twog0 = 2 * g.g0;
+    const bool fast = (g.g1 % 2 == 0) && (g.npad % 2 == 0) && (item_lo % twog0 == 0) &&
+                      (item_hi % twog0 == 0) && g.nrow >= g.g0 && g.ncol >= g.g1;
+    if (fast) {
+        const int64_t j_lo = item_lo / g.g0;
+        const int64_t npairs = (item_hi / g.g0 - j_lo) / 2;
+        const int64_t rows = ceil_div(g.nrow, g.g0);  // max owned rows
+        const int64_t base = g.g0 * npairs;
+        const int64_t cols = ceil_div(g.ncol, g.g1);
+        // chunks of at least max(1, kMinChunkDraws / cols) rows
+        const int64_t min_rows = std::max<int64_t>(1, kMinChunkDraws / std::max<int64_t>(1, cols));
+        int64_t nchunks = std::max<int64_t>(1, std::min(ceil_div(kTargetUnits, base),
+                                                          ceil_div(rows, min_rows)));
+        const int64_t rpc = ceil_div(rows, nchunks);
+        nchunks = ceil_div(rows, rpc);
+        const int64_t nunits = base * nchunks;
+        fill_uniform_fast<KIND><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
+            cur, out, g, j_lo, npairs, rpc, nunits, rate, tab);
+        return launch_check("fill_uniform_fast");
+    }
+    const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
+    int64_t chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * nloc, kTargetUnits));
+    chunk = std::min(chunk, std::max<int64_t>(1, maxdraws));
+    const int64_t nunits = nloc * ceil_div(maxdraws, chunk);
+    fill_uniform_generic<KIND><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
+        cur, out, g, item_lo, nloc, chunk, nunits, rate, tab);
+    return launch_check("fill_uniform_generic");
+}
+
+template <typename T>
+static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, int64_t item_hi,
+                         cudaStream_t st) {
+    Pow2Table tab;
+    pow2_table(&tab);
+    const int64_t pair_lo = item_lo / 2, pair_hi = item_hi / 2;
+    const int64_t nloc = pair_hi - pair_lo;
+    if (nloc == 0) return SFB_OK;
+    const int64_t half = g.g1 / 2;
+    const bool fast = (g.npad % 2 == 0) && (pair_lo % half == 0) && (pair_hi % half == 0) &&
+                      g.nrow >= g.g0 && g.ncol >= g.g1;
+    if (fast) {
+        const int64_t i_lo = pair_lo / half;
+        const int64_t nrows_grid = (pair_hi - pair_lo) / half;
+        const int64_t rows = ceil_div(g.nrow, g.g0);
+        const int64_t base = nrows_grid * half;
+        const int64_t cols = ceil_div(g.ncol, g.g1);
+        const int64_t min_rows = std::max<int64_t>(1, kMinChunkDraws / std::max<int64_t>(1, cols));
+        int64_t nchunks = std::max<int64_t>(1, std::min(ceil_div(kTargetUnits, base),
+                                                          ceil_div(rows, min_rows)));
+        const int64_t rpc = ceil_div(rows, nchunks);
+        nchunks = ceil_div(rows, rpc);
+        const int64_t nunits = base * nchunks;
+        fill_normal_fast<T><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
+            cur, out, g, i_lo, nrows_grid, rpc, nunits, tab);
+        return launch_check("fill_normal_fast");
+    }
+    const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
+    int64_t chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * nloc, kTargetUnits));
+    chunk = std::min(chunk, std::max<int64_t>(1, maxdraws));
+    const int64_t nunits = nloc * ceil_div(maxdraws, chunk);
+    fill_normal_generic<T><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
+        cur, out, g, pair_lo, nloc, chunk, nunits, tab);
+    return launch_check("fill_normal_generic");
+}
+
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" {
+
+int sfb_device_ok(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return 0;
+    }
+    int dev = 0, major = 0, minor = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major == 10 && minor == 0;
+}
+
+int sfb_fill_real(int64_t *d_cur, int64_t n_streams, double *d_out, int64_t nrow, int64_t ncol,
+                  int64_t npad, int64_t g0, int64_t g1, int mode, double rate, int64_t item_lo,
+                  int64_t item_hi, int zero_pad, void *stream) {
+    if (int rc = check_common(n_streams, nrow, ncol, npad, g0, g1, item_lo, item_hi)) return rc;
+    if (mode != 0 && mode != 1) return fail(SFB_E_INVALID_ARGUMENT, "unknown fill mode %d", mode);
+    if (mode == 1 && !(rate > 0)) return fail(SFB_E_INVALID_RATE, "exponential rate must be > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (zero_pad)
+        if (int rc = zero_padding(d_out, sizeof(double), nrow, ncol, npad, st)) return rc;
+    const Geom g{nrow, ncol, npad, g0, g1};
+    return mode == 0 ? launch_uniform<kUniform>(d_cur, d_out, g, item_lo, item_hi, rate, st)
+                     : launch_uniform<kExponential>(d_cur, d_out, g, item_lo, item_hi, rate, st);
+}
+
+int sfb_fill_integer(int64_t *d_cur, int64_t n_streams, int64_t *d_out, int64_t nrow,
+                     int64_t ncol, int64_t npad, int64_t g0, int64_t g1, int64_t item_lo,
+                     int64_t item_hi, int zero_pad, void *stream) {
+    if (int rc = check_common(n_streams, nrow, ncol, npad, g0, g1, item_lo, item_hi)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (zero_pad)
+        if (int rc = zero_padding(d_out, sizeof(int64_t), nrow, ncol, npad, st)) return rc;
+    const Geom g{nrow, ncol, npad, g0, g1};
+    return launch_uniform<kInteger>(d_cur, d_out, g, item_lo, item_hi, 1.0, st);
+}
+
+int sfb_fill_normal(int64_t *d_cur, int64_t n_streams, void *d_out, int out_dtype, int64_t nrow,
+                    int64_t ncol, int64_t npad, int64_t g0, int64_t g1, int64_t item_lo,
+                    int64_t item_hi, int zero_pad, void *stream) {
+    if (int rc = check_common(n_streams, nrow, ncol, npad, g0, g1, item_lo, item_hi)) return rc;
+    if (g1 % 2 != 0)
+        return fail(SFB_E_INVALID_GRID, "normal generation needs an even lane count (nglobal1)");
+    if (item_lo % 2 != 0 || item_hi % 2 != 0)
+        return fail(SFB_E_INVALID_ARGUMENT, "normal shard range must be pair aligned");
+    if (out_dtype != SFB_F64 && out_dtype != SFB_F32)
+        return fail(SFB_E_INVALID_ARGUMENT, "normal output dtype must be f64 or f32");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t es = out_dtype == SFB_F64 ? sizeof(double) : sizeof(float);
+    if (zero_pad)
+        if (int rc = zero_padding(d_out, es, nrow, ncol, npad, st)) return rc;
+    const Geom g{nrow, ncol, npad, g0, g1};
+    if (out_dtype == SFB_F64)
+        return launch_normal<double>(d_cur, (double *)d_out, g, item_lo, item_hi, st);
+    return launch_normal<float>(d_cur, (float *)d_out, g, item_lo, item_hi, st);
+}
+
+}  // extern "C"

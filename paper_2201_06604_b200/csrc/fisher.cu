@@ -1,0 +1,397 @@
+// fisher.cu -- sm_100a Monte Carlo Fisher exact test (fisher.sim).
+//
+// Reference: _kernels.fisher_replicates (_kernels.py:169-286) driven by
+// fisher.fisher_sim (fisher.py:118-164), and _kernels.rcont2_table
+// (_kernels.py:289-391).  Every replicate samples an I x J table with the
+// observed margins by sequential conditional hypergeometric inversion, one
+// uniform per free cell (exactly (I-1)(J-1) steps, _kernels.py:210-212),
+// scores stat = -sum lf[n_ij] row-major and counts stat <= threshold.
+//
+// Bit-exactness:
+//   * this TU is compiled with -fmad=false: the reference's numba loop has no
+//     FMA contraction, so every mul/add/div below is a separately rounded
+//     IEEE op in the reference's order (division is IEEE round-to-nearest);
+//   * exp() is the glibc FMA-variant port (exp_glibc.cuh);
+//   * lf is the host scipy gammaln table, uploaded, never recomputed;
+//   * the statistic is accumulated cell by cell in exactly the row-major order
+//     of _kernels.py:271-274 (rows 0..I-2 as they are sampled, then the last
+//     row), so no table is ever materialised.
+//
+// Parallel decomposition: replicate r of item w starts at
+// A^(r F) s_w with F = (I-1)(J-1).  Replicates of an item are split into
+// `nchunks` chunks of `rpc` replicates; the start-state jumps A^(c rpc F) are
+// computed exactly on the host and passed by value.  A unit (item, chunk) is
+// one thread; adjacent lanes are adjacent items of the same chunk, so the
+// per-cell control flow is warp-uniform except for the CDF walk.  Hits are
+// reduced warp-shuffle -> shared memory -> one 64-bit atomic per CTA; the
+// multi-GPU layer then does one NCCL all-reduce of that count.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "exp_glibc.cuh"
+#include "sfb_internal.h"
+
+namespace sfb {
+
+constexpr int kMaxChunks = 96;
+constexpr int kFisherThreads = 256;
+
+struct ChunkJumps {
+    Jump j[kMaxChunks];
+};
+
+struct FisherArgs {
+    int64_t *cur;
+    const int32_t *rowm;  // device margins (int32; totals < 2^31 checked)
+    const int32_t *colm;
+    const double *lf;
+    double *stats;
+    int64_t *item_counts;
+    unsigned long long *count;
+    double threshold;
+    int64_t item_lo, nloc, reps, rpc, nunits;
+    int nr, nc, ntot, lf_len;
+};
+
+// one conditional hypergeometric draw (_kernels.py:205-261); consumes one step
+template <typename LF>
+__device__ __forceinline__ int sample_cell(int ia, int idv, int ie, int ib, int ic, int ii,
+                                           const LF &lf, const uint64_t *exptab, Mrg &s) {
+    const uint32_t z = step(s);  // _kernels.py:211
+    const double u = (double)z * kNorm;
+    int lo = ia + idv - ie;
+    if (lo < 0) lo = 0;
+    const int hi = ia < idv ? ia : idv;
+    if (hi <= lo) return lo;  // forced cell: the uniform is still consumed
+    // start the CDF inversion near the mode (_kernels.py:221-225)
+    int k = (int)((double)ia * ((double)idv / (double)ie) + 0.5);
+    if (k < lo)
+        k = lo;
+    else if (k > hi)
+        k = hi;
+    const double base = lf(ia) + lf(ib) + lf(idv) + lf(ic) - lf(ie);  // :226
+    const double x = glibc_exp(base - lf(k) - lf(idv - k) - lf(ia - k) - lf(ii + k), exptab);
+    if (!(u > x)) return k;
+    // walk outward, alternating up and down (_kernels.py:230-261)
+    double acc = x, pu = x, pd = x;
+    int ku = k, kd = k;
+    for (;;) {
+        bool moved = false;
+        if (ku < hi) {
+            pu = pu * (double)(idv - ku) * (double)(ia - ku) /
+                 (((double)ku + 1.0) * ((double)(ii + ku) + 1.0));
+            ku += 1;
+            acc += pu;
+            moved = true;
+            if (u <= acc) return ku;
+        }
+        if (kd > lo) {
+            pd = pd * (double)kd * (double)(ii + kd) /
+                 (((double)(idv - kd) + 1.0) * ((double)(ia - kd) + 1.0));
+            kd -= 1;
+            acc += pd;
+            moved = true;
+            if (u <= acc) return kd;
+        }
+        if (!moved) return ku;  // round-off leftover: take an endpoint
+    }
+}
+
+// sample one table and return its statistic; jw = per-thread column work
+// array (stride `js`), mat (nullable) receives the table (rcont2)
+template <typename LF>
+__device__ __forceinline__ double sample_table(const int32_t *rowm, const int32_t *colm, int nr,
+                                               int nc, int ntot, const LF &lf,
+                                               const uint64_t *exptab, Mrg &s, int *jw, int js,
+                                               int64_t *mat) {
+    double stat = 0.0;
+    int jc = ntot;
+    for (int m = 0; m < nc - 1; ++m) jw[m * js] = colm[m];
+    for (int l = 0; l < nr - 1; ++l) {
+        int ia = rowm[l];
+        int ic = jc;
+        jc -= ia;
+        for (int m = 0; m < nc - 1; ++m) {
+            const int idv = jw[m * js];
+            const int ie = ic;
+            ic -= idv;
+            const int ib = ie - ia;
+            const int ii = ib - idv;
+            const int k = sample_cell(ia, idv, ie, ib, ic, ii, lf, exptab, s);
+            stat -= lf(k);  // row-major order of _kernels.py:271-274
+            if (mat) mat[l * nc + m] = k;
+            ia -= k;
+            jw[m * js] = idv - k;
+        }
+        stat -= lf(ia);  // mat[l, nc-1] = ia
+        if (mat) mat[l * nc + nc - 1] = ia;
+    }
+    int rem = rowm[nr - 1];
+    for (int m = 0; m < nc - 1; ++m) {
+        const int v = jw[m * js];
+        stat -= lf(v);
+        if (mat) mat[(nr - 1) * nc + m] = v;
+        rem -= v;
+    }
+    stat -= lf(rem);
+    if (mat) mat[(nr - 1) * nc + nc - 1] = rem;
+    return stat;
+}
+
+struct LfGlobal {
+    const double *p;
+    __device__ __forceinline__ double operator()(int k) const { return __ldg(p + k); }
+};
+struct LfShared {
+    const double *p;
+    __device__ __forceinline__ double operator()(int k) const { return p[k]; }
+};
+
+// dynamic shared memory: exp table (2 KiB) | margins | [lf] | jwork
+template <bool LF_SMEM>
+__global__ void __launch_bounds__(kFisherThreads) fisher_kernel(const FisherArgs a,
+                                                         const __grid_constant__ ChunkJumps jumps) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t *exptab = (uint64_t *)smem;
+    int32_t *rowm = (int32_t *)(exptab + 256);
+    int32_t *colm = rowm + a.nr;
+    double *lfs = (double *)(((uintptr_t)(colm + a.nc) + 15) & ~(uintptr_t)15);
+    int *jwork = LF_SMEM ? (int *)(lfs + a.lf_len) : (int *)lfs;
+
+    static const uint64_t kTab[256] = SFB_EXP_TABLE_INIT;
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) exptab[t] = kTab[t];
+    for (int t = threadIdx.x; t < a.nr; t += blockDim.x) rowm[t] = a.rowm[t];
+    for (int t = threadIdx.x; t < a.nc; t += blockDim.x) colm[t] = a.colm[t];
+    if (LF_SMEM)
+        for (int t = threadIdx.x; t < a.lf_len; t += blockDim.x) lfs[t] = a.lf[t];
+    __syncthreads();
+
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int hits = 0;
+    if (u < a.nunits) {
+        const int64_t local = u % a.nloc;
+        const int64_t c = u / a.nloc;
+        const int64_t w = a.item_lo + local;
+        const int64_t rep0 = c * a.rpc;
+        const int64_t rep1 = min(rep0 + a.rpc, a.reps);
+        if (rep0 < rep1) {
+            Mrg s = load_state(a.cur + 6 * w);
+            if (c) apply(jumps.j[c], s);
+            int *jw = jwork + threadIdx.x;
+            for (int64_t rep = rep0; rep < rep1; ++rep) {
+                double stat;
+                if (LF_SMEM)
+                    stat = sample_table(rowm, colm, a.nr, a.nc, a.ntot, LfShared{lfs}, exptab, s,
+                                        jw, blockDim.x, nullptr);
+                else
+                    stat = sample_table(rowm, colm, a.nr, a.nc, a.ntot, LfGlobal{a.lf}, exptab,
+                                        s, jw, blockDim.x, nullptr);
+                if (stat <= a.threshold) ++hits;  // _kernels.py:275-276
+                if (a.stats) a.stats[local * a.reps + rep] = stat;
+            }
+            if (rep1 == a.reps) store_state(a.cur + 6 * w, s);
+            if (a.item_counts) atomicAdd((unsigned long long *)(a.item_counts + local),
+                                         (unsigned long long)hits);
+        }
+    }
+    // warp shuffle -> shared -> one atomic per CTA
+    __shared__ int warp_sums[kFisherThreads / 32];
+    const int ws = __reduce_add_sync(0xffffffffu, hits);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = ws;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int v = threadIdx.x < (blockDim.x >> 5) ? warp_sums[threadIdx.x] : 0;
+        v = __reduce_add_sync(0xffffffffu, v);
+        if (threadIdx.x == 0 && v) atomicAdd(a.count, (unsigned long long)v);
+    }
+}
+
+__global__ void rcont2_kernel(const int32_t *rowm, const int32_t *colm, int nr, int nc, int ntot,
+                              const double *lf, int64_t *state, int64_t *mat) {
+    static const uint64_t kTab[256] = SFB_EXP_TABLE_INIT;
+    __shared__ uint64_t exptab[256];
+    for (int t = 0; t < 256; ++t) exptab[t] = kTab[t];
+    extern __shared__ int jw[];
+    Mrg s = load_state(state);
+    if (nr == 1) {  // _kernels.py:307-312: forced without draws
+        for (int m = 0; m < nc; ++m) mat[m] = colm[m];
+    } else if (nc == 1) {
+        for (int l = 0; l < nr; ++l) mat[l] = rowm[l];
+    } else {
+        sample_table(rowm, colm, nr, nc, ntot, LfGlobal{lf}, exptab, s, jw, 1, mat);
+    }
+    store_state(state, s);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static int check_margins(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
+                         const double *lf, int64_t lf_len, int *ntot_out) {
+    if (nr < 1 || nc < 1) return fail(SFB_E_INVALID_MARGINS, "margins must be 1-D and non-empty");
+    int64_t sr = 0, sc = 0;
+    for (int l = 0; l < nr; ++l) {
+        if (nrowt[l] < 0) return fail(SFB_E_INVALID_MARGINS, "margins must be non-negative");
+        sr += nrowt[l];
+    }
+    for (int m = 0; m < nc; ++m) {
+        if (ncolt[m] < 0) return fail(SFB_E_INVALID_MARGINS, "margins must be non-negative");
+        sc += ncolt[m];
+    }
+    if (sr != sc) return fail(SFB_E_INVALID_MARGINS, "row and column margins have different totals");
+    if (sr >= (1LL << 31) - 1)
+        return fail(SFB_E_INVALID_ARGUMENT, "table total %lld exceeds the int32 device range",
+                    (long long)sr);
+    if (!lf || lf_len < sr + 1)
+        return fail(SFB_E_INVALID_ARGUMENT, "log-factorial table needs total+1 = %lld entries",
+                    (long long)(sr + 1));
+    *ntot_out = (int)sr;
+    return SFB_OK;
+}
+
+struct DeviceScratch {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    ~DeviceScratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+// stage margins (int32) and lf in one stream-ordered device allocation
+static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
+                        const double *lf, int64_t lf_len, cudaStream_t st, DeviceScratch &scr,
+                        int32_t **rowm, int32_t **colm, double **lfd) {
+    const size_t lf_off = ((size_t)(nr + nc) * 4 + 15) & ~(size_t)15;
+    const size_t bytes = lf_off + (size_t)lf_len * 8;
+    std::vector<unsigned char> host(bytes);
+    int32_t *hr = (int32_t *)host.data();
+    for (int l = 0; l < nr; ++l) hr[l] = (int32_t)nrowt[l];
+    for (int m = 0; m < nc; ++m) hr[nr + m] = (int32_t)ncolt[m];
+    memcpy(host.data() + lf_off, lf, (size_t)lf_len * 8);
+    scr.st = st;
+    cudaError_t e = cudaMallocAsync(&scr.p, bytes, st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
+    e = cudaMemcpyAsync(scr.p, host.data(), bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "margins upload: %s", cudaGetErrorString(e));
+    // pageable source: make sure the staging copy finished before `host` dies
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "margins upload: %s", cudaGetErrorString(e));
+    *rowm = (int32_t *)scr.p;
+    *colm = *rowm + nr;
+    *lfd = (double *)((unsigned char *)scr.p + lf_off);
+    return SFB_OK;
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" {
+
+int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrowt, int nr,
+                          const int64_t *ncolt, int nc, const double *lf, int64_t lf_len,
+                          double threshold, int64_t reps, int64_t item_lo, int64_t item_hi,
+                          double *d_stats, int64_t *d_item_counts, uint64_t *d_count,
+                          int zero_count, void *stream) {
+    int ntot = 0;
+    if (int rc = check_margins(nrowt, nr, ncolt, nc, lf, lf_len, &ntot)) return rc;
+    if (reps < 0) return fail(SFB_E_INVALID_ARGUMENT, "reps must be >= 0");
+    if (item_lo < 0 || item_hi < item_lo || item_hi > n_streams)
+        return fail(SFB_E_INSUFFICIENT_STREAMS, "item range [%lld, %lld) needs %lld streams, got %lld",
+                    (long long)item_lo, (long long)item_hi, (long long)item_hi,
+                    (long long)n_streams);
+    if (!d_count) return fail(SFB_E_INVALID_ARGUMENT, "count output is required");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (zero_count) {
+        e = cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st);
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "count memset: %s", cudaGetErrorString(e));
+    }
+    const int64_t nloc = item_hi - item_lo;
+    if (d_item_counts && nloc) {
+        e = cudaMemsetAsync(d_item_counts, 0, sizeof(int64_t) * nloc, st);
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "item count memset: %s", cudaGetErrorString(e));
+    }
+    if (nloc == 0 || reps == 0) return SFB_OK;
+
+    DeviceScratch scr;
+    int32_t *rowm, *colm;
+    double *lfd;
+    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, scr, &rowm, &colm, &lfd))
+        return rc;
+
+    // chunking: enough units to fill the machine, bounded by kMaxChunks
+    const int64_t F = (int64_t)(nr - 1) * (nc - 1);
+    constexpr int64_t kTarget = 148LL * 2048 * 2;
+    int64_t nchunks = std::min<int64_t>({(int64_t)kMaxChunks, reps, ceil_div(kTarget, nloc)});
+    if (F == 0) nchunks = 1;  // degenerate tables consume no draws
+    nchunks = std::max<int64_t>(1, nchunks);
+    const int64_t rpc = ceil_div(reps, nchunks);
+    nchunks = ceil_div(reps, rpc);
+    ChunkJumps jumps;
+    for (int64_t c = 0; c < nchunks; ++c) jump_pow((uint64_t)(c * rpc * F), &jumps.j[c]);
+
+    FisherArgs a;
+    a.cur = d_cur;
+    a.rowm = rowm;
+    a.colm = colm;
+    a.lf = lfd;
+    a.stats = d_stats;
+    a.item_counts = d_item_counts;
+    a.count = (unsigned long long *)d_count;
+    a.threshold = threshold;
+    a.item_lo = item_lo;
+    a.nloc = nloc;
+    a.reps = reps;
+    a.rpc = rpc;
+    a.nunits = nloc * nchunks;
+    a.nr = nr;
+    a.nc = nc;
+    a.ntot = ntot;
+    a.lf_len = (int)lf_len;
+
+    const size_t head = 2048 + (size_t)(nr + nc) * 4 + 16;
+    const size_t jw = (size_t)std::max(nc - 1, 1) * kFisherThreads * 4;
+    const size_t lf_bytes = (size_t)lf_len * 8;
+    const bool lf_smem = head + lf_bytes + jw <= 110 * 1024;
+    const size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
+    const unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
+    if (smem > 200 * 1024) return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
+    if (lf_smem) {
+        e = cudaFuncSetAttribute(fisher_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e == cudaSuccess)
+            fisher_kernel<true><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    } else {
+        e = cudaFuncSetAttribute(fisher_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e == cudaSuccess)
+            fisher_kernel<false><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher kernel launch: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc, const double *lf,
+                     int64_t lf_len, int64_t *d_state, int64_t *d_mat, void *stream) {
+    int ntot = 0;
+    if (int rc = check_margins(nrowt, nr, ncolt, nc, lf, lf_len, &ntot)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceScratch scr;
+    int32_t *rowm, *colm;
+    double *lfd;
+    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, scr, &rowm, &colm, &lfd))
+        return rc;
+    rcont2_kernel<<<1, 1, (size_t)std::max(nc, 1) * 4, st>>>(rowm, colm, nr, nc, ntot, lfd,
+                                                              d_state, d_mat);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "rcont2 launch: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,436 @@
+// host_streams.cpp -- host side of libsfb: exact stream arithmetic, stream
+// files, error plumbing and CPU test hooks.
+//
+// Replaces the pure-Python big-integer code of the reference (core.py):
+//   _mat_mul/_jump_matrices/_mat_vec   core.py:48-66
+//   next_state / jump_ahead            core.py:114-136
+//   _jump_seed / create_streams        core.py:139-142, 222-235
+//   save_streams / save_streams_atomic core.py:238-261
+//   load_streams (+ StreamSet.validate) core.py:264-305, 204-212
+// All arithmetic is exact (uint64 accumulators, entries < 2^31), so results
+// equal the reference's Python ints bit for bit.
+#include <errno.h>
+#include <fcntl.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+#include <mutex>
+#include <string>
+
+#include "exp_glibc.cuh"
+#include "sfb_internal.h"
+
+namespace sfb {
+
+static thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+// _T1 / _T2 of core.py:44-45 (acting on (x[n-1], x[n-2], x[n-3]))
+static const uint32_t kT1[9] = {0, 1u << 22, (1u << 7) + 1, 1, 0, 0, 0, 1, 0};
+static const uint32_t kT2[9] = {1u << 15, 0, (1u << 15) + 1, 1, 0, 0, 0, 1, 0};
+
+static void mat_mul(const Mat3 &a, const Mat3 &b, uint32_t mod, Mat3 &o) {
+    Mat3 t;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            uint64_t acc = 0;
+            for (int k = 0; k < 3; ++k) acc += (uint64_t)a.m[3 * i + k] * b.m[3 * k + j];
+            t.m[3 * i + j] = (uint32_t)(acc % mod);
+        }
+    o = t;
+}
+
+static Jump identity_jump() {
+    Jump j;
+    for (int k = 0; k < 9; ++k) j.p1.m[k] = j.p2.m[k] = (k % 4 == 0) ? 1u : 0u;
+    return j;
+}
+
+static Jump base_jump() {
+    Jump j;
+    memcpy(j.p1.m, kT1, sizeof kT1);
+    memcpy(j.p2.m, kT2, sizeof kT2);
+    return j;
+}
+
+static void jump_mul(const Jump &a, const Jump &b, Jump &o) {
+    mat_mul(a.p1, b.p1, kM1, o.p1);
+    mat_mul(a.p2, b.p2, kM2, o.p2);
+}
+
+void jump_pow2(int e, Jump *out) {  // core.py:55-62
+    Jump j = base_jump();
+    for (int k = 0; k < e; ++k) jump_mul(j, j, j);
+    *out = j;
+}
+
+void jump_pow(uint64_t n, Jump *out) {
+    Jump r = identity_jump(), p = base_jump();
+    while (n) {
+        if (n & 1) jump_mul(p, r, r);  // powers of A commute
+        n >>= 1;
+        if (n) jump_mul(p, p, p);
+    }
+    *out = r;
+}
+
+void pow2_table(Pow2Table *t) {
+    static std::once_flag once;
+    static Pow2Table cached;
+    std::call_once(once, [] {
+        Jump j = base_jump();
+        for (int b = 0; b < kPow2Bits; ++b) {
+            cached.p[b] = j;
+            jump_mul(j, j, j);
+        }
+    });
+    *t = cached;
+}
+
+static const uint64_t kExpTable[256] = SFB_EXP_TABLE_INIT;
+
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" {
+
+const char *sfb_last_error(void) { return g_err.c_str(); }
+
+int sfb_version(void) { return 100; }
+
+int sfb_validate_seed(const int64_t seed[6]) {  // core.py:69-86
+    for (int c = 0; c < 2; ++c) {
+        const int64_t *v = seed + 3 * c;
+        const int64_t m = c == 0 ? kM1 : kM2;
+        for (int k = 0; k < 3; ++k)
+            if (v[k] < 0 || v[k] >= m)
+                return fail(SFB_E_INVALID_SEED, "component-%d seed component %lld outside [0, %lld]",
+                            c + 1, (long long)v[k], (long long)(m - 1));
+        if (v[0] == 0 && v[1] == 0 && v[2] == 0)
+            return fail(SFB_E_INVALID_SEED, "component-%d seed must not be all zero", c + 1);
+    }
+    return SFB_OK;
+}
+
+int sfb_next_state(int64_t state[6], int64_t *z) {  // core.py:114-123
+    // exact int64 restatement (inputs may be any valid state)
+    const int64_t M1 = kM1, M2 = kM2;
+    int64_t y1 = ((1LL << 22) * state[1] + 129LL * state[2]) % M1;
+    int64_t y2 = ((1LL << 15) * state[3] + 32769LL * state[5]) % M2;
+    state[2] = state[1];
+    state[1] = state[0];
+    state[0] = y1;
+    state[5] = state[4];
+    state[4] = state[3];
+    state[3] = y2;
+    int64_t zz = ((y1 - y2) % M1 + M1) % M1;
+    *z = zz == 0 ? M1 : zz;
+    return SFB_OK;
+}
+
+int sfb_jump_matrices(int e, int64_t j1[9], int64_t j2[9]) {
+    if (e < 0) return fail(SFB_E_INVALID_ARGUMENT, "jump exponent must be >= 0");
+    Jump j;
+    jump_pow2(e, &j);
+    for (int k = 0; k < 9; ++k) {
+        j1[k] = j.p1.m[k];
+        j2[k] = j.p2.m[k];
+    }
+    return SFB_OK;
+}
+
+static void apply_i64(const Jump &j, int64_t s[6]) {
+    Mrg m = load_state(s);
+    apply(j, m);
+    store_state(s, m);
+}
+
+static int check_state(const int64_t s[6]) {
+    for (int k = 0; k < 6; ++k) {
+        const int64_t m = k < 3 ? kM1 : kM2;
+        if (s[k] < 0 || s[k] >= m)
+            return fail(SFB_E_INVALID_ARGUMENT, "state component %lld outside [0, %lld]",
+                        (long long)s[k], (long long)(m - 1));
+    }
+    return SFB_OK;
+}
+
+int sfb_jump_ahead(int64_t state[6], int e) {  // core.py:126-136
+    if (e < 0) return fail(SFB_E_INVALID_ARGUMENT, "jump exponent must be >= 0");
+    if (int rc = check_state(state)) return rc;
+    Jump j;
+    jump_pow2(e, &j);
+    apply_i64(j, state);
+    return SFB_OK;
+}
+
+int sfb_skip(int64_t state[6], uint64_t n) {
+    if (int rc = check_state(state)) return rc;
+    Jump j;
+    jump_pow(n, &j);
+    apply_i64(j, state);
+    return SFB_OK;
+}
+
+int sfb_create_streams(const int64_t seed[6], int64_t n, int64_t *rows,
+                       int64_t next_seed[6]) {  // core.py:222-235
+    if (n < 1) return fail(SFB_E_INVALID_ARGUMENT, "number of streams to create must be >= 1");
+    if (int rc = sfb_validate_seed(seed)) return rc;
+    static std::once_flag once;
+    static Jump j134;
+    std::call_once(once, [] { jump_pow2(134, &j134); });
+    Mrg s = load_state(seed);
+    for (int64_t k = 0; k < n; ++k) {
+        store_state(rows + 6 * k, s);
+        apply(j134, s);  // _jump_seed, core.py:139-142
+    }
+    store_state(next_seed, s);
+    return SFB_OK;
+}
+
+/* ---- stream files -------------------------------------------------------- */
+static const char kMagic[] = "streamforge-streams";  // core.py:238
+static const char kVersion[] = "v1";                 // core.py:239
+
+int64_t sfb_format_streams_bound(int64_t n) { return 96 + n * 12 * 21; }
+
+static char *put_i64(char *p, int64_t v) {
+    char tmp[24];
+    int k = 0;
+    uint64_t u = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+    do {
+        tmp[k++] = (char)('0' + u % 10);
+        u /= 10;
+    } while (u);
+    if (v < 0) *p++ = '-';
+    while (k) *p++ = tmp[--k];
+    return p;
+}
+
+int sfb_format_streams(const int64_t *current, const int64_t *initial, int64_t n,
+                       char *buf, int64_t cap, int64_t *len) {  // core.py:242-250
+    if (cap < sfb_format_streams_bound(n))
+        return fail(SFB_E_INVALID_ARGUMENT, "format buffer too small");
+    char *p = buf;
+    p += snprintf(p, 96, "%s %s count=%lld\n", kMagic, kVersion, (long long)n);
+    for (int64_t k = 0; k < n; ++k) {
+        for (int c = 0; c < 12; ++c) {
+            if (c) *p++ = ' ';
+            p = put_i64(p, c < 6 ? current[6 * k + c] : initial[6 * k + c - 6]);
+        }
+        *p++ = '\n';
+    }
+    *len = p - buf;
+    return SFB_OK;
+}
+
+int sfb_save_streams(const char *path, const int64_t *current, const int64_t *initial,
+                     int64_t n, int atomic) {  // core.py:242-261
+    const int64_t cap = sfb_format_streams_bound(n);
+    char *buf = (char *)malloc((size_t)cap);
+    if (!buf) return fail(SFB_E_IO, "out of memory formatting %lld streams", (long long)n);
+    int64_t len = 0;
+    int rc = sfb_format_streams(current, initial, n, buf, cap, &len);
+    if (rc) {
+        free(buf);
+        return rc;
+    }
+    std::string target = path;
+    std::string tmp = atomic ? target + ".tmp" : target;
+    int fd = open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+    if (fd < 0) {
+        free(buf);
+        return fail(SFB_E_IO, "%s: %s", tmp.c_str(), strerror(errno));
+    }
+    int64_t off = 0;
+    while (off < len) {
+        ssize_t w = write(fd, buf + off, (size_t)(len - off));
+        if (w < 0) {
+            if (errno == EINTR) continue;
+            int e = errno;
+            close(fd);
+            free(buf);
+            return fail(SFB_E_IO, "%s: %s", tmp.c_str(), strerror(e));
+        }
+        off += w;
+    }
+    free(buf);
+    if (atomic && fsync(fd) != 0) {
+        int e = errno;
+        close(fd);
+        return fail(SFB_E_IO, "fsync %s: %s", tmp.c_str(), strerror(e));
+    }
+    if (close(fd) != 0) return fail(SFB_E_IO, "close %s: %s", tmp.c_str(), strerror(errno));
+    if (atomic && rename(tmp.c_str(), target.c_str()) != 0)
+        return fail(SFB_E_IO, "rename %s: %s", tmp.c_str(), strerror(errno));
+    return SFB_OK;
+}
+
+// Python str.split() whitespace (ASCII subset)
+static inline bool is_ws(char c) {
+    return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f' ||
+           (c >= 0x1c && c <= 0x1f);
+}
+
+struct Cursor {
+    const char *p, *end;
+    // next line without its '\n' terminator (file.readline semantics);
+    // returns false at EOF (readline() == "")
+    bool line(const char *&b, const char *&e) {
+        if (p >= end) return false;
+        b = p;
+        const char *nl = (const char *)memchr(p, '\n', (size_t)(end - p));
+        e = nl ? nl : end;
+        p = nl ? nl + 1 : end;
+        return true;
+    }
+};
+
+// split [b, e) on whitespace into at most maxtok tokens; returns the count
+// (maxtok + 1 means "more than maxtok")
+static int split(const char *b, const char *e, const char **tb, const char **te, int maxtok) {
+    int n = 0;
+    while (b < e) {
+        while (b < e && is_ws(*b)) ++b;
+        if (b >= e) break;
+        const char *s = b;
+        while (b < e && !is_ws(*b)) ++b;
+        if (n == maxtok) return maxtok + 1;
+        tb[n] = s;
+        te[n] = b;
+        ++n;
+    }
+    return n;
+}
+
+// Python int(token): optional sign, digits with single '_' separators
+static bool parse_int(const char *b, const char *e, int64_t *out) {
+    bool neg = false;
+    if (b < e && (*b == '+' || *b == '-')) neg = *b++ == '-';
+    if (b >= e || *b < '0' || *b > '9') return false;
+    unsigned __int128 v = 0;
+    bool prev_digit = false;
+    for (; b < e; ++b) {
+        if (*b == '_') {
+            if (!prev_digit || b + 1 >= e || b[1] < '0' || b[1] > '9') return false;
+            prev_digit = false;
+            continue;
+        }
+        if (*b < '0' || *b > '9') return false;
+        v = v * 10 + (unsigned)(*b - '0');
+        if (v > ((unsigned __int128)1 << 64)) return false;
+        prev_digit = true;
+    }
+    if (neg) {
+        if (v > ((unsigned __int128)1 << 63)) return false;
+        *out = (int64_t)(0 - (uint64_t)v);
+    } else {
+        if (v >= ((unsigned __int128)1 << 63)) return false;
+        *out = (int64_t)v;
+    }
+    return true;
+}
+
+static int parse_header(Cursor &cur, int64_t *count) {  // core.py:271-284
+    const char *b, *e;
+    if (!cur.line(b, e)) b = e = cur.p;
+    const char *tb[4], *te[4];
+    int nt = split(b, e, tb, te, 3);
+    if (nt != 3 || (size_t)(te[0] - tb[0]) != strlen(kMagic) ||
+        memcmp(tb[0], kMagic, strlen(kMagic)) != 0 ||
+        (size_t)(te[1] - tb[1]) != strlen(kVersion) ||
+        memcmp(tb[1], kVersion, strlen(kVersion)) != 0 || te[2] - tb[2] < 6 ||
+        memcmp(tb[2], "count=", 6) != 0)
+        return fail(SFB_E_CORRUPT_STREAM_FILE, "bad stream file header");
+    int64_t n;
+    if (!parse_int(tb[2] + 6, te[2], &n))
+        return fail(SFB_E_CORRUPT_STREAM_FILE, "bad stream count in header");
+    if (n < 1) return fail(SFB_E_CORRUPT_STREAM_FILE, "stream count must be >= 1");
+    *count = n;
+    return SFB_OK;
+}
+
+int sfb_parse_streams_count(const char *text, int64_t len, int64_t *n) {
+    Cursor cur{text, text + len};
+    return parse_header(cur, n);
+}
+
+int sfb_parse_streams(const char *text, int64_t len, int64_t *current, int64_t *initial,
+                      int64_t n) {  // core.py:264-305
+    Cursor cur{text, text + len};
+    int64_t count;
+    if (int rc = parse_header(cur, &count)) return rc;
+    if (count != n) return fail(SFB_E_INVALID_ARGUMENT, "count mismatch");
+    for (int64_t k = 0; k < count; ++k) {
+        const char *b, *e;
+        if (!cur.line(b, e))
+            return fail(SFB_E_CORRUPT_STREAM_FILE, "truncated file: expected %lld streams",
+                        (long long)count);
+        const char *tb[13], *te[13];
+        if (split(b, e, tb, te, 12) != 12)
+            return fail(SFB_E_CORRUPT_STREAM_FILE, "stream %lld: expected 12 integers",
+                        (long long)(k + 1));
+        for (int c = 0; c < 12; ++c) {
+            int64_t v;
+            if (!parse_int(tb[c], te[c], &v))
+                return fail(SFB_E_CORRUPT_STREAM_FILE, "stream %lld: non-integer entry",
+                            (long long)(k + 1));
+            (c < 6 ? current[6 * k + c] : initial[6 * k + c - 6]) = v;
+        }
+    }
+    const char *b, *e;
+    if (cur.line(b, e)) {
+        for (; b < e; ++b)
+            if (!is_ws(*b)) return fail(SFB_E_CORRUPT_STREAM_FILE, "trailing data after last stream");
+    }
+    // StreamSet.validate (core.py:204-212): ranges first for both arrays, then
+    // all-zero triplets, in the reference's order
+    const int64_t *arrs[2] = {current, initial};
+    const char *what[2] = {"current", "initial"};
+    for (int a = 0; a < 2; ++a)
+        for (int side = 0; side < 2; ++side) {
+            const int64_t m = side == 0 ? kM1 : kM2;
+            for (int64_t k = 0; k < count; ++k)
+                for (int c = 0; c < 3; ++c) {
+                    int64_t v = arrs[a][6 * k + 3 * side + c];
+                    if (v < 0 || v >= m)
+                        return fail(SFB_E_CORRUPT_STREAM_FILE, "%s state integer outside [0, %lld]",
+                                    what[a], (long long)(m - 1));
+                }
+            for (int64_t k = 0; k < count; ++k) {
+                const int64_t *t = arrs[a] + 6 * k + 3 * side;
+                if (t[0] == 0 && t[1] == 0 && t[2] == 0)
+                    return fail(SFB_E_CORRUPT_STREAM_FILE, "all-zero %s state triplet", what[a]);
+            }
+        }
+    return SFB_OK;
+}
+
+/* ---- CPU test hooks -------------------------------------------------------- */
+int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out) {
+    for (int64_t w = 0; w < n; ++w) {
+        Mrg s = load_state(states + 6 * w);
+        for (int64_t t = 0; t < steps; ++t) {
+            uint32_t z = step(s);
+            if (z_out) z_out[w * steps + t] = z;
+        }
+        store_state(states + 6 * w, s);
+    }
+    return SFB_OK;
+}
+
+double sfb_host_exp(double x) { return glibc_exp(x, kExpTable); }
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// mrg31k3p.cuh -- MRG31k3p arithmetic shared by host and device code.
+//
+// Reference: the int64 step `_step` (_kernels.py:33-47) and its oracle
+// `next_state` (core.py:114-123):
+//   y1 = (2^22*a1 + (2^7+1)*a2) mod m1, shift (a0,a1,a2) <- (y1,a0,a1)
+//   y2 = (2^15*b0 + (2^15+1)*b2) mod m2, shift (b0,b1,b2) <- (y2,b0,b1)
+//   z  = y1 - y2, z <= 0 => z += m1          (z in [1, m1])
+//
+// B200 formulation: everything in uint32 registers, no 64-bit multiply.
+//   component 1: for x < m1 = 2^31-1, 2^k x mod m1 is the 31-bit rotation
+//     rot31(x, k), which is again < m1; so y1 = rot22(a1) + rot7(a2) + a2 with
+//     two conditional subtractions (each sum stays < 2^32).
+//   component 2: with t = b0 + b2 (< 2^32), 2^15 t = (t>>16) 2^31 + (t&0xffff) 2^15
+//     and 2^31 == 21069 (mod m2), so 2^15 t == (t>>16)*21069 + ((t&0xffff)<<15)
+//     (< 2^32), one conditional subtraction, then + b2 and one more.
+// Conditional subtraction is min(v, v - m) on unsigned values (v < 2m).
+// Verified against the int64 oracle step on random and extreme states by the
+// CPU test tests/test_host_lib.py (through sfb_host_step_u32).
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define SFB_HD __host__ __device__ __forceinline__
+#else
+#define SFB_HD inline
+#endif
+
+namespace sfb {
+
+constexpr uint32_t kM1 = 2147483647u;  // core.py:29
+constexpr uint32_t kM2 = 2147462579u;  // core.py:30
+constexpr double kNorm = 1.0 / 2147483648.0;  // _kernels.py:20
+
+SFB_HD uint32_t umin32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return min(a, b);
+#else
+    return a < b ? a : b;
+#endif
+}
+
+SFB_HD uint32_t csub(uint32_t v, uint32_t m) { return umin32(v, v - m); }
+
+struct Mrg {
+    uint32_t a0, a1, a2, b0, b1, b2;
+};
+
+// one MRG31k3p step (_kernels.py:33-47); returns z in [1, m1]
+SFB_HD uint32_t step(Mrg &s) {
+    const uint32_t r22 = ((s.a1 << 22) & kM1) | (s.a1 >> 9);
+    const uint32_t r7 = ((s.a2 << 7) & kM1) | (s.a2 >> 24);
+    uint32_t y1 = csub(r22 + r7, kM1);
+    y1 = csub(y1 + s.a2, kM1);
+    s.a2 = s.a1;
+    s.a1 = s.a0;
+    s.a0 = y1;
+    const uint32_t t = s.b0 + s.b2;
+    uint32_t y2 = csub((t >> 16) * 21069u + ((t & 0xffffu) << 15), kM2);
+    y2 = csub(y2 + s.b2, kM2);
+    s.b2 = s.b1;
+    s.b1 = s.b0;
+    s.b0 = y2;
+    return y1 > y2 ? y1 - y2 : y1 - y2 + kM1;
+}
+
+SFB_HD Mrg load_state(const int64_t *row) {
+    Mrg s;
+    s.a0 = (uint32_t)row[0];
+    s.a1 = (uint32_t)row[1];
+    s.a2 = (uint32_t)row[2];
+    s.b0 = (uint32_t)row[3];
+    s.b1 = (uint32_t)row[4];
+    s.b2 = (uint32_t)row[5];
+    return s;
+}
+
+SFB_HD void store_state(int64_t *row, const Mrg &s) {
+    row[0] = s.a0;
+    row[1] = s.a1;
+    row[2] = s.a2;
+    row[3] = s.b0;
+    row[4] = s.b1;
+    row[5] = s.b2;
+}
+
+// 3x3 modular matrix (row-major) acting on (x[n-1], x[n-2], x[n-3]) --
+// the transition matrices _T1/_T2 of core.py:44-45 and their powers.
+struct Mat3 {
+    uint32_t m[9];
+};
+
+// a*v0 + b*v1 + c*v2 mod m: three 62-bit products sum below 2^64
+SFB_HD uint32_t dot3_mod(const uint32_t *row, uint32_t v0, uint32_t v1, uint32_t v2,
+                         uint32_t mod) {
+    const uint64_t acc = (uint64_t)row[0] * v0 + (uint64_t)row[1] * v1 + (uint64_t)row[2] * v2;
+    return (uint32_t)(acc % mod);
+}
+
+SFB_HD void apply1(const Mat3 &p, uint32_t &x0, uint32_t &x1, uint32_t &x2) {
+    const uint32_t y0 = dot3_mod(p.m + 0, x0, x1, x2, kM1);
+    const uint32_t y1 = dot3_mod(p.m + 3, x0, x1, x2, kM1);
+    const uint32_t y2 = dot3_mod(p.m + 6, x0, x1, x2, kM1);
+    x0 = y0;
+    x1 = y1;
+    x2 = y2;
+}
+
+SFB_HD void apply2(const Mat3 &p, uint32_t &x0, uint32_t &x1, uint32_t &x2) {
+    const uint32_t y0 = dot3_mod(p.m + 0, x0, x1, x2, kM2);
+    const uint32_t y1 = dot3_mod(p.m + 3, x0, x1, x2, kM2);
+    const uint32_t y2 = dot3_mod(p.m + 6, x0, x1, x2, kM2);
+    x0 = y0;
+    x1 = y1;
+    x2 = y2;
+}
+
+// A^n for both components as one jump: state <- (P1 g1, P2 g2)
+struct Jump {
+    Mat3 p1, p2;
+};
+
+SFB_HD void apply(const Jump &j, Mrg &s) {
+    apply1(j.p1, s.a0, s.a1, s.a2);
+    apply2(j.p2, s.b0, s.b1, s.b2);
+}
+
+// Powers A^(2^b), b < kPow2Bits, for device-side arbitrary skip-ahead.
+constexpr int kPow2Bits = 48;
+struct Pow2Table {
+    Jump p[kPow2Bits];
+};
+
+// advance s by n < 2^kPow2Bits steps (binary powering; bit-exact for any n)
+SFB_HD void skip(const Pow2Table &t, Mrg &s, uint64_t n) {
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+    for (int b = 0; n != 0 && b < kPow2Bits; ++b, n >>= 1)
+        if (n & 1) apply(t.p[b], s);
+}
+
+}  // namespace sfb

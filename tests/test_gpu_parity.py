@@ -1,0 +1,435 @@
+"""GPU parity: the sm_100a kernels (through the package API / C ABI) against
+the reference-generated goldens and the CPU oracle.
+
+Bars:
+  * uniforms, integers, stream states, Fisher counts / statistics / states:
+    bit-exact;
+  * Box-Muller float64: |gpu - ref| <= 8 ulp(ref) relative, or 2^-52 absolute
+    near zero crossings (CUDA log/cos vs glibc log/cos);
+  * Box-Muller float32: |gpu - float32(ref)| <= 1 ulp_f32 everywhere, and
+    identical on >= 99.999 % of cells;
+  * exponential: |gpu - ref| <= 4 ulp(ref) (CUDA log1p vs glibc log1p).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2201_06604_b200 as sf
+from conftest import SIM_1, sha
+from oracle import oracle as orc
+import oracle_api as oa
+
+pytestmark = pytest.mark.gpu
+
+
+def fresh(n):
+    return sf.create_streams(sf.set_base_creator(), n)[0]
+
+
+def grid(g):
+    return sf.WorkGrid(*g)
+
+
+def ulp64(x):
+    return np.spacing(np.abs(x).astype(np.float64))
+
+
+def assert_normal_f64_close(got, ref):
+    err = np.abs(got - ref)
+    tol = np.maximum(8 * ulp64(ref), 2.0 ** -52)
+    bad = err > tol
+    assert not bad.any(), (got[bad][:5], ref[bad][:5], err.max())
+
+
+def assert_normal_f32_close(got, ref64):
+    ref = ref64.astype(np.float32)
+    same = got == ref
+    ulp = np.spacing(np.abs(ref))
+    assert (np.abs(got.astype(np.float64) - ref.astype(np.float64)) <= ulp).all()
+    assert same.mean() >= 0.99999, same.mean()
+
+
+# ---------------------------------------------------------------- uniforms
+def test_sim1_published_vector(G):
+    st = fresh(4)
+    v = sf.fill_uniform(st, sf.FillRequest(shape=8, grid=sf.WorkGrid(2, 2))).vector()
+    assert tuple(np.round(v, 3)) == SIM_1
+    assert v.tolist() == G["sim_1"]["values"]
+    assert st.current.tolist() == G["sim_1"]["states"]
+
+
+UNI = ["U1a", "U1b", "U1c", "U1d", "Upad", "Uodd", "Uodd_int", "Uragged", "Uvec_odd",
+       "Uwide", "Ubig"]
+
+
+@pytest.mark.parametrize("name", UNI)
+def test_uniform_goldens_bit_exact(G, A, name):
+    g = G[name]
+    st = fresh(g["n_streams"])
+    shape = g["shape"] if isinstance(g["shape"], int) else tuple(g["shape"])
+    buf = sf.fill_uniform(st, sf.FillRequest(shape=shape, kind=g["kind"], grid=grid(g["grid"]),
+                                             npad=g["npad"] if g["npad"] != (
+                                                 shape if isinstance(shape, int)
+                                                 else shape[1]) else None))
+    assert sha(buf.data) == g["data_sha"]
+    assert sha(st.current) == g["states_sha"]
+    if name + "_data" in A:
+        assert np.array_equal(buf.data, A[name + "_data"])
+
+
+def test_single_item_grid_matches_sequential_stepping():
+    st = fresh(4)
+    buf = sf.fill_uniform(st, sf.FillRequest(shape=12, grid=sf.WorkGrid(1, 1)))
+    s = sf.create_streams(sf.set_base_creator(), 1)[0][0]
+    outs = []
+    for _ in range(12):
+        s, z = sf.next_state(s)
+        outs.append(z)
+    assert np.array_equal(buf.vector(), np.array(outs) * sf.NORM)
+
+
+def test_unused_streams_unchanged_and_padding_zero():
+    st = fresh(10)
+    before = st.current.copy()
+    buf = sf.run_grid(st, sf.WorkGrid(2, 2), 3, 3, "uniform", npad=5)
+    assert np.array_equal(buf.data[:, 3:], np.zeros((3, 2)))
+    assert (buf.values != 0).all()
+    assert np.array_equal(st.current[4:], before[4:])
+    assert not np.array_equal(st.current[:4], before[:4])
+
+
+@pytest.mark.parametrize("shape,g,n", [
+    ((1, 1), (1, 1), 1), ((5, 7), (2, 3), 6), ((129, 257), (4, 6), 24),
+    ((64, 64), (64, 64), 4096), ((3, 1000), (2, 512), 1024), (100001, (1, 512), 512),
+    ((250, 250), (16, 2), 32), ((17, 4096), (3, 64), 192), ((2048, 2048), (32, 32), 1024),
+])
+@pytest.mark.parametrize("kind", ["uniform", "uniform-integer"])
+def test_uniform_layouts_vs_oracle(shape, g, n, kind):
+    st = fresh(n)
+    buf = sf.fill_uniform(st, sf.FillRequest(shape=shape, kind=kind, grid=sf.WorkGrid(*g)))
+    ref_st = oa.fresh_states(n)
+    ref = oa.fill(kind, ref_st, shape, g)
+    assert np.array_equal(buf.data, ref)
+    assert np.array_equal(st.current, ref_st)
+
+
+def test_repeated_calls_chain_on_device():
+    # device mirror: two fills without touching .current == one longer fill
+    st = fresh(64)
+    a = sf.fill_uniform(st, sf.FillRequest(shape=(64, 64), grid=sf.WorkGrid(8, 8)))
+    b = sf.fill_uniform(st, sf.FillRequest(shape=(64, 64), grid=sf.WorkGrid(8, 8)))
+    st2 = fresh(64)
+    c = sf.fill_uniform(st2, sf.FillRequest(shape=(128, 64), grid=sf.WorkGrid(8, 8)))
+    assert np.array_equal(np.vstack([a.data, b.data]), c.data)
+    assert st == st2
+
+
+def test_host_edits_between_calls_are_honoured():
+    st = fresh(4)
+    sf.fill_uniform(st, sf.FillRequest(shape=8, grid=sf.WorkGrid(2, 2)))
+    st.current[0] = [12345] * 6  # in-place edit by the caller
+    v = sf.fill_uniform(st, sf.FillRequest(shape=2, grid=sf.WorkGrid(1, 1))).vector()
+    assert v[0] == G_first()
+
+
+def G_first():
+    return 0.7353244530968368
+
+
+def test_ks_uniform():
+    from scipy import stats
+
+    st = fresh(64)
+    v = sf.fill_uniform(st, sf.FillRequest(shape=100_000, grid=sf.WorkGrid(8, 8))).vector()
+    d = stats.kstest(v, "uniform").statistic
+    assert d < math.sqrt(-math.log(0.0005) / 2) / math.sqrt(100_000)
+    assert v.min() > 0 and v.max() < 1
+
+
+# ----------------------------------------------------------------- normals
+NRM = ["N64", "N34", "Nodd", "Nodd2", "Nvec"]
+
+
+@pytest.mark.parametrize("name", NRM)
+def test_normal_goldens_within_tolerance(G, A, name):
+    g = G[name]
+    shape = g["shape"] if isinstance(g["shape"], int) else tuple(g["shape"])
+    ncol = shape if isinstance(shape, int) else shape[1]
+    npad = g["npad"] if g["npad"] != ncol else None
+    st = fresh(g["n_streams"])
+    buf = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=grid(g["grid"]), npad=npad))
+    ref = A[name + "_data"]
+    assert_normal_f64_close(buf.data, ref)
+    assert sha(st.current) == g["states_sha"]
+    st = fresh(g["n_streams"])
+    b32 = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=grid(g["grid"]), npad=npad,
+                                            dtype=np.float32))
+    assert b32.data.dtype == np.float32
+    assert_normal_f32_close(b32.data, ref)
+    assert sha(st.current) == g["states_sha"]
+
+
+@pytest.mark.parametrize("name", ["N1", "Nwide"])
+def test_normal_large_vs_oracle(G, name):
+    g = G[name]
+    shape = tuple(g["shape"])
+    st = fresh(g["n_streams"])
+    buf = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=grid(g["grid"])))
+    ref_st = oa.fresh_states(g["n_streams"])
+    ref = oa.fill("normal", ref_st, shape, tuple(g["grid"]))
+    assert sha(ref) == g["data_sha"]
+    assert_normal_f64_close(buf.data, ref)
+    assert np.array_equal(st.current, ref_st)
+    st = fresh(g["n_streams"])
+    b32 = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=grid(g["grid"]),
+                                            dtype=np.float32))
+    assert_normal_f32_close(b32.data, ref)
+
+
+@pytest.mark.parametrize("shape,g,n", [
+    ((3, 3), (1, 2), 2), ((7, 9), (2, 4), 8), ((100, 101), (4, 10), 40),
+    ((64, 1000), (8, 512), 4096), ((31250 // 50, 32000 // 50), (16, 16), 256),
+])
+def test_normal_layouts_vs_oracle(shape, g, n):
+    st = fresh(n)
+    buf = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=sf.WorkGrid(*g)))
+    ref_st = oa.fresh_states(n)
+    ref = oa.fill("normal", ref_st, shape, g)
+    assert_normal_f64_close(buf.data, ref)
+    assert np.array_equal(st.current, ref_st)
+
+
+def test_box_muller_pair_identity():
+    g = sf.WorkGrid(4, 4)
+    st = fresh(16)
+    v = sf.fill_normal(st, sf.FillRequest(shape=(64, 64), grid=g)).values
+    ref_st = oa.fresh_states(16)
+    u = oa.fill("uniform", ref_st.copy(), (64, 64), (4, 4))  # not the pair stream map
+    del u
+    x, y = v[:, 0::2], v[:, 1::2]
+    r2 = x * x + y * y
+    assert np.isfinite(r2).all() and (r2 > 0).all()
+
+
+def test_normal_moments():
+    st = fresh(64)
+    v = sf.fill_normal(st, sf.FillRequest(shape=(1000, 1000), grid=sf.WorkGrid(8, 8))).values
+    v = v.ravel()
+    assert -0.004 < v.mean() < 0.004
+    assert 0.994 < v.var() < 1.006
+
+
+def test_odd_width_discards_partner_but_advances_both():
+    st = fresh(2)
+    before = st.copy()
+    sf.fill_normal(st, sf.FillRequest(shape=(2, 3), grid=sf.WorkGrid(1, 2)))
+    for w in range(2):
+        s = before[w]
+        for _ in range(4):
+            s, _ = sf.next_state(s)
+        assert st[w].g1 == s.g1
+
+
+# ------------------------------------------------------------- exponential
+@pytest.mark.parametrize("rate", [0.5, 1.0, 2.0])
+def test_exponential_small(G, rate):
+    st = fresh(4)
+    buf = sf.fill_exponential(st, sf.FillRequest(shape=(2, 4), kind="exponential", rate=rate,
+                                                 grid=sf.WorkGrid(2, 2)))
+    ref = np.array(G[f"E24_{rate}"]["values"])
+    assert (np.abs(buf.values - ref) <= 4 * ulp64(ref)).all()
+    assert st.current.tolist() == G[f"E24_{rate}"]["states"]
+
+
+def test_exponential_big(A):
+    st = fresh(16)
+    buf = sf.fill_exponential(st, sf.FillRequest(shape=(100, 100), kind="exponential",
+                                                 rate=1.5, grid=sf.WorkGrid(4, 4)))
+    ref = A["E100_data"]
+    assert (np.abs(buf.data - ref) <= 4 * ulp64(ref)).all()
+    assert np.array_equal(st.current, A["E100_states"])
+
+
+# ------------------------------------------------------------------ Fisher
+def _tables(G, A):
+    t = {"T4": np.array(G["T4"]), "T10": np.array(G["T10"]), "month": A["month"],
+         "week": A["week"]}
+    for k in list(A):
+        if k.startswith("tab_"):
+            t[k[4:]] = A[k]
+    return t
+
+
+FIS = ["F_T4_1e6", "F_T10_1e6", "F_month_1e6", "F_week_1e6", "F_month_2e5", "F_month_s",
+       "F_T4_s", "F_T10_s", "F_week_s", "F_2x2_s", "F_E2x2", "F_E2x5", "F_E5x2",
+       "F_Ezero_col", "F_Eones", "F_Ebig", "F_week_1e7"]
+
+
+@pytest.mark.parametrize("key", FIS)
+def test_fisher_goldens_bit_exact(G, A, key):
+    g = G[key]
+    tabs = _tables(G, A)
+    st = fresh(g["n_streams"])
+    want = key + "_stats" in A
+    r = sf.fisher_sim(tabs[g["table"]], g["n"], st, grid=grid(g["grid"]), return_stats=want)
+    assert r.sim_num == g["sim_num"]
+    assert r.counts == g["counts"]
+    assert r.p_value == g["p_value"]
+    assert r.threshold == g["threshold"]
+    assert sha(st.current) == g["states_sha"]
+    if want:
+        assert np.array_equal(r.statistics, A[key + "_stats"])
+
+
+def test_fisher_rerun_and_chunk_invariance(A):
+    # replicate chunking depends on the item count; results must not
+    month = A["month"]
+    base = None
+    for g in [(1, 1), (2, 2), (4, 4), (16, 16)]:
+        n_items = g[0] * g[1]
+        st = fresh(n_items)
+        r = sf.fisher_sim(month, 4096, st, grid=sf.WorkGrid(*g), return_stats=True)
+        ref_st = oa.fresh_states(n_items)
+        ref = oa.fisher(month, 4096, ref_st, g, return_stats=True)
+        assert r.counts == ref["counts"]
+        assert np.array_equal(r.statistics, ref["statistics"])
+        assert np.array_equal(st.current, ref_st)
+        if base is None:
+            base = r.counts
+
+
+def test_fisher_stream_advancement_audit(A):
+    st = fresh(4)
+    before = st.copy()
+    r = sf.fisher_sim(A["month"], 8, st, grid=sf.WorkGrid(2, 2))
+    reps = r.sim_num // 4
+    for w in range(4):
+        s = sf.skip_ahead(before[w], reps * 121)
+        assert st[w].g1 == s.g1 and st[w].g2 == s.g2
+
+
+def test_fisher_item_shards_compose(G, A):
+    # the multi-GPU decomposition on one device: disjoint item ranges
+    import torch
+
+    from paper_2201_06604_b200.fisher import launch_fisher, plan_fisher
+
+    t10 = np.array(G["T10"])
+    st = fresh(16384)
+    plan = plan_fisher(t10, 10 ** 6, st, sf.WorkGrid(256, 64))
+    cur = st.device_current()
+    total = 0
+    for lo, hi in [(0, 5000), (5000, 5001), (5001, 16384)]:
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        launch_fisher(plan, cur, st.count, cnt, item_lo=lo, item_hi=hi)
+        total += int(cnt.item())
+    st._mark_device_ahead()
+    assert total == G["F_T10_1e6"]["counts"]
+    assert sha(st.current) == G["F_T10_1e6"]["states_sha"]
+
+
+def test_fisher_t10_sampled_items_many_reps(G):
+    # C4 shape: per-item counts/final states for sampled items at 4769 reps
+    import torch
+
+    from paper_2201_06604_b200.fisher import launch_fisher, plan_fisher
+
+    t10 = np.array(G["T10"])
+    n_items = 1 << 14
+    st = fresh(n_items)
+    plan = plan_fisher(t10, 4769 * n_items, st, sf.WorkGrid(128, 128))
+    assert plan.reps == 4769
+    rng = np.random.default_rng(5)
+    items = np.sort(rng.choice(n_items, 12, replace=False))
+    cur = st.device_current()
+    ic = torch.zeros(n_items, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    launch_fisher(plan, cur, st.count, cnt, item_counts_dev=ic)
+    st._mark_device_ahead()
+    ic = ic.cpu().numpy()
+    assert ic.sum() == int(cnt.item())
+    ref_st = oa.fresh_states(n_items)
+    for w in items:
+        item_counts = np.zeros(1, np.int64)
+        orc.fisher_replicates(ref_st, t10.sum(1), t10.sum(0), plan.lf, plan.kernel_threshold,
+                              plan.reps, int(w) + 1, item_lo=int(w), item_counts=item_counts)
+        assert ic[w] == item_counts[0]
+        assert np.array_equal(st.current[w], ref_st[w])
+
+
+def test_rcont2_goldens(G, A):
+    month = A["month"]
+    t = sf.ContingencyTable(month)
+    lf = sf.fisher.log_factorial_table(t.total)
+    state = np.array([12345] * 6, np.int64)
+    tabs = [sf.rcont2(t.row_margins, t.col_margins, state, lf) for _ in range(5)]
+    assert np.array_equal(np.array(tabs), A["rcont2_month5"])
+    assert state.tolist() == G["rcont2_month5_state"]
+    state = np.array([12345] * 6, np.int64)
+    assert sf.rcont2([7], [2, 2, 3], state).tolist() == [[2, 2, 3]]
+    assert state.tolist() == [12345] * 6
+    state = np.array([12345] * 6, np.int64)
+    t10 = sf.rcont2([20000, 8000, 3000, 1000, 400, 150, 60, 25, 10, 5],
+                    [13000, 9000, 5000, 2500, 1200, 1000, 600, 250, 75, 25], state)
+    assert t10.tolist() == G["T10"]
+
+
+def test_2x2_converges_to_exact_fisher_p():
+    from scipy.special import gammaln
+
+    def pmf(k, ia, idv, ie):
+        return math.exp(gammaln(ia + 1) + gammaln(ie - ia + 1) + gammaln(idv + 1)
+                        + gammaln(ie - idv + 1) - gammaln(ie + 1) - gammaln(k + 1)
+                        - gammaln(idv - k + 1) - gammaln(ia - k + 1)
+                        - gammaln(ie - ia - idv + k + 1))
+
+    table = np.array([[3, 7], [6, 2]])
+    obs = sf.logfact_sum(table)
+    total, ia, idv = 18, 10, 9
+    exact = 0.0
+    for k in range(max(0, ia + idv - total), min(ia, idv) + 1):
+        cand = np.array([[k, ia - k], [idv - k, total - ia - idv + k]])
+        if sf.logfact_sum(cand) <= sf.fisher.relaxed_threshold(obs):
+            exact += pmf(k, ia, idv, total)
+    res = sf.fisher_sim(table, 10 ** 6, fresh(64), grid=sf.WorkGrid(8, 8))
+    se = math.sqrt(exact * (1 - exact) / res.sim_num)
+    assert abs(res.p_value - exact) < 3 * se
+
+
+# -------------------------------------------------------------- checkpoint
+def test_checkpoint_continuation_c5_64(G, tmp_path):
+    import torch
+
+    g = sf.WorkGrid(128, 128)
+    st = fresh(1 << 14)
+    a = sf.run_grid(st, g, 4096, 8192, "uniform")
+    p = tmp_path / "ckpt.txt"
+    sf.save_streams_atomic(st, p)
+    st2 = sf.load_streams(p)
+    b = sf.run_grid(st2, g, 4096, 8192, "uniform")
+    full = torch.cat([a.tensor, b.tensor]).cpu().numpy()
+    assert sha(full) == G["C5_64"]["full_sha"]
+    assert sha(st2.current) == G["C5_64"]["states_sha"]
+
+
+@pytest.mark.slow
+def test_checkpoint_continuation_c5_full(tmp_path):
+    # C5 at full size on the device: 2^20 streams x 4096 uniforms (34.4 GB),
+    # checkpoint after rows [0, 32768), resume -> identical bytes and states
+    import torch
+
+    g = sf.WorkGrid(1024, 1024)
+    st_full = fresh(1 << 20)
+    full = sf.run_grid(st_full, g, 65536, 65536, "uniform")
+    st = fresh(1 << 20)
+    a = sf.run_grid(st, g, 32768, 65536, "uniform")
+    assert torch.equal(a.tensor, full.tensor[:32768])
+    del a
+    p = tmp_path / "c5.txt"
+    sf.save_streams_atomic(st, p)
+    st2 = sf.load_streams(p)
+    b = sf.run_grid(st2, g, 32768, 65536, "uniform")
+    assert torch.equal(b.tensor, full.tensor[32768:])
+    assert st2 == st_full

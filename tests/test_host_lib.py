@@ -1,0 +1,328 @@
+"""CPU tests of the product's host half and of the device arithmetic run on the
+host: libsfb.so loads and exports every symbol of include/sfb.h, the uint32
+MRG31k3p formulation equals the int64 reference step, the glibc exp port is
+bit-exact against libm, the stream arithmetic / stream files match the
+reference-generated goldens, and the API validates like the reference."""
+
+import ctypes
+import ctypes.util
+import io
+import math
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2201_06604_b200 as sf
+from paper_2201_06604_b200 import _lib
+from paper_2201_06604_b200.errors import (
+    CorruptStreamFileError,
+    DeviceError,
+    InsufficientStreamsError,
+    InvalidArgumentError,
+    InvalidGridError,
+    InvalidMarginsError,
+    InvalidRateError,
+    InvalidSeedError,
+)
+from paper_2201_06604_b200.fisher import (
+    ContingencyTable,
+    log_factorial_table,
+    relaxed_threshold,
+    sim_num_for,
+)
+
+from conftest import PRINTED_STREAM_MATRIX, ROOT, has_gpu, sha
+from oracle import oracle as orc
+
+
+def test_library_exports_every_header_symbol():
+    header = open(os.path.join(ROOT, "include", "sfb.h")).read()
+    declared = set(re.findall(r"\b(sfb_[a-z0-9_]+)\s*\(", header))
+    assert declared == set(_lib.EXPORTED)
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert _lib.lib().sfb_version() >= 100
+
+
+def test_sm100a_only_binary():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out, out
+
+
+def _u32_step(states, steps):
+    s = np.ascontiguousarray(states.copy())
+    z = np.zeros(len(s) * steps, np.int64)
+    _lib.check(_lib.lib().sfb_host_step_u32(_lib.ptr(s), len(s), steps, _lib.ptr(z)))
+    return s, z.reshape(len(s), steps)
+
+
+def _oracle_steps(states, steps):
+    s = states.copy()
+    z = np.zeros((len(s), steps), np.int64)
+    for w in range(len(s)):
+        row = np.ascontiguousarray(s[w])
+        for t in range(steps):
+            z[w, t] = orc.step(row)
+        s[w] = row
+    return s, z
+
+
+def test_u32_step_matches_int64_reference_step():
+    rng = np.random.default_rng(1)
+    n = 400
+    st = np.empty((n, 6), np.int64)
+    st[:, :3] = rng.integers(0, sf.M1, size=(n, 3))
+    st[:, 3:] = rng.integers(0, sf.M2, size=(n, 3))
+    # extreme states: all components at the top of their range, zeros, ones
+    st[0] = [sf.M1 - 1] * 3 + [sf.M2 - 1] * 3
+    st[1] = [0, 0, 1, 0, 0, 1]
+    st[2] = [1, 0, 0, 1, 0, 0]
+    st[3] = [sf.M1 - 1, 0, sf.M1 - 1, sf.M2 - 1, 0, sf.M2 - 1]
+    st[4] = [2 ** 30, 2 ** 30 - 1, 2 ** 31 - 2, 2 ** 30, 2 ** 31 - 21070, 2 ** 16]
+    a, za = _u32_step(st, 300)
+    b, zb = _oracle_steps(st, 300)
+    assert np.array_equal(za, zb)
+    assert np.array_equal(a, b)
+
+
+def _libm_exp():
+    libm = ctypes.CDLL(ctypes.util.find_library("m"))
+    libm.exp.argtypes = [ctypes.c_double]
+    libm.exp.restype = ctypes.c_double
+    return libm.exp
+
+
+def _bits(x):
+    return struct.unpack("<Q", struct.pack("<d", x))[0]
+
+
+def test_exp_table_matches_host_libm():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "gen_exp_data", os.path.join(ROOT, "paper_2201_06604_b200", "csrc", "gen_exp_data.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    consts, tab = mod.extract()
+    inc = open(os.path.join(ROOT, "paper_2201_06604_b200", "csrc", "exp_data.inc")).read()
+    words = [int(w, 16) for w in re.findall(r"0x([0-9a-f]{16})ull,", inc)]
+    assert words == list(tab)
+    for name, c in zip(mod.NAMES, consts):
+        m = re.search(rf"SFB_EXP_{name}_BITS 0x([0-9a-f]{{16}})ull", inc)
+        assert int(m.group(1), 16) == _bits(c)
+
+
+def test_exp_port_bit_exact_against_libm():
+    libm_exp = _libm_exp()
+    port = _lib.lib().sfb_host_exp
+    rng = np.random.default_rng(7)
+    xs = list(rng.uniform(-5.0, 0.0, 60000))          # the Fisher argument range
+    xs += list(rng.uniform(-745.5, 709.9, 30000))     # full finite range incl. specialcase
+    xs += list(-np.exp(rng.uniform(-60, 2, 10000)))   # tiny to moderate negatives
+    xs += list(rng.uniform(-1100, 1100, 2000))        # overflow / underflow
+    xs += [0.0, -0.0, 1e-300, -1e-300, 2.0 ** -54, -(2.0 ** -54), 2.0 ** -55, 511.999,
+           -511.999, 512.0, -512.0, 700.0, -700.0, 709.78, 709.79, -708.4, -708.5, -744.0,
+           -745.1, -745.2, -746.0, 1024.0, -1024.0, math.inf, -math.inf, math.nan,
+           5e-324, -5e-324, 1.0, -1.0]
+    bad = [x for x in xs if _bits(port(x)) != _bits(libm_exp(x))
+           and not (math.isnan(port(x)) and math.isnan(libm_exp(x)))]
+    assert not bad, bad[:10]
+
+
+def test_printed_matrix_and_goldens(G):
+    s4 = sf.create_streams(sf.set_base_creator(), 4)[0]
+    assert np.array_equal(s4.matrix(), PRINTED_STREAM_MATRIX)
+    st, c = sf.create_streams(sf.set_base_creator(), 1 << 20)
+    assert sha(st.current) == G["create_2p20"]["sha"]
+    assert list(c.next_seed) == G["create_2p20"]["next_seed"]
+    st, c = sf.create_streams(sf.set_base_creator((11, 22, 33, 44, 55, 66)), 300)
+    assert sha(st.current) == G["create_toy_300"]["sha"]
+    assert np.array_equal(st.current, st.initial)
+
+
+@pytest.mark.parametrize("e", [0, 1, 10, 134])
+def test_jump_matrices(G, e):
+    j1, j2 = sf.core._jump_matrices(e)
+    assert [list(r) for r in j1] == G[f"jump_{e}"]["j1"]
+    assert [list(r) for r in j2] == G[f"jump_{e}"]["j2"]
+
+
+def test_next_state_and_jumps(G):
+    s = sf.StreamState.from_seed(sf.DEFAULT_SEED)
+    outs = []
+    s0 = s
+    for _ in range(2000):
+        s, z = sf.next_state(s)
+        outs.append(z)
+    assert sha(np.array(outs, np.int64)) == G["next_state_2000"]["outs_sha"]
+    assert list(s.g1 + s.g2) == G["next_state_2000"]["final"]
+    assert s.initial_g1 == (12345,) * 3
+    j = sf.jump_ahead(s0, 134)
+    assert j.g1 == (336690377, 597094797, 1245771585)
+    assert j.g2 == (85196284, 523477687, 2094976052)
+    t = sf.StreamState.from_seed((11, 22, 33, 44, 55, 66))
+    for e in range(12):
+        stepped = t
+        for _ in range(2 ** e):
+            stepped, _ = sf.next_state(stepped)
+        assert sf.jump_ahead(t, e).g1 == stepped.g1
+        assert sf.skip_ahead(t, 2 ** e).g2 == stepped.g2
+    with pytest.raises(InvalidArgumentError):
+        sf.jump_ahead(s0, -1)
+
+
+def test_creator_validation():
+    assert sf.set_base_creator().next_seed == (12345,) * 6
+    for bad in [(0, 0, 0, 1, 1, 1), (sf.M1, 1, 1, 1, 1, 1), (1, 1, 1, sf.M2, 1, 1),
+                (-1, 1, 1, 1, 1, 1), (1, 2, 3)]:
+        with pytest.raises(InvalidSeedError):
+            sf.set_base_creator(bad)
+    with pytest.raises(InvalidArgumentError):
+        sf.create_streams(sf.set_base_creator(), 0)
+    a, c = sf.create_streams(sf.set_base_creator(), 2)
+    b, _ = sf.create_streams(c, 2)
+    full, _ = sf.create_streams(sf.set_base_creator(), 4)
+    assert np.array_equal(np.vstack([a.current, b.current]), full.current)
+
+
+def test_stream_file_format(G, tmp_path):
+    s3 = sf.create_streams(sf.set_base_creator(), 3)[0]
+    buf = io.StringIO()
+    sf.save_streams(s3, buf)
+    assert buf.getvalue() == G["save_3"]
+    back = sf.load_streams(io.StringIO(buf.getvalue()))
+    assert back == s3
+    p = tmp_path / "s.txt"
+    sf.save_streams(s3, str(p))
+    assert p.read_text() == G["save_3"]
+    sf.save_streams_atomic(s3, p)
+    assert p.read_text() == G["save_3"]
+    assert not os.path.exists(str(p) + ".tmp")
+    assert sf.load_streams(str(p)) == s3
+    # negative / arbitrary int64 values are formatted like Python str(int)
+    arr = np.array([[1, -2, 3, 4, 5, 6]], np.int64)
+    odd = sf.StreamSet(arr, arr.copy())
+    buf = io.StringIO()
+    sf.save_streams(odd, buf)
+    assert buf.getvalue().splitlines()[1] == "1 -2 3 4 5 6 1 -2 3 4 5 6"
+
+
+@pytest.mark.parametrize("content", [
+    "",
+    "wrong-magic v1 count=1\n" + " ".join(["1"] * 12),
+    "streamforge-streams v2 count=1\n" + " ".join(["1"] * 12),
+    "streamforge-streams v1 count=2\n" + " ".join(["1"] * 12) + "\n",
+    "streamforge-streams v1 count=1\n1 2 3\n",
+    "streamforge-streams v1 count=1\n" + " ".join(["x"] * 12) + "\n",
+    "streamforge-streams v1 count=0\n",
+    "streamforge-streams v1 count=x\n",
+    "streamforge-streams v1 count=1\n" + " ".join(["1"] * 12) + "\nextra\n",
+    "streamforge-streams v1 count=1\n" + " ".join(["0"] * 12) + "\n",
+    "streamforge-streams v1 count=1\n" + " ".join([str(sf.M1)] + ["1"] * 11) + "\n",
+])
+def test_malformed_files_rejected(content):
+    with pytest.raises(CorruptStreamFileError):
+        sf.load_streams(io.StringIO(content))
+
+
+def test_parser_accepts_python_int_forms():
+    text = ("streamforge-streams v1 count=+1\n"
+            "1 0_2 +3 4 5 6 1 2 3 4 5 6\n\n")
+    s = sf.load_streams(io.StringIO(text))
+    assert s.current.tolist() == [[1, 2, 3, 4, 5, 6]]
+
+
+def test_round_trip_property():
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 17):
+        cur = np.empty((n, 6), np.int64)
+        cur[:, :3] = rng.integers(1, sf.M1, (n, 3))
+        cur[:, 3:] = rng.integers(1, sf.M2, (n, 3))
+        s = sf.StreamSet(cur.copy(), cur.copy())
+        buf = io.StringIO()
+        sf.save_streams(s, buf)
+        assert sf.load_streams(io.StringIO(buf.getvalue())) == s
+
+
+def test_checkpoint_files_at_c5_scale(tmp_path):
+    # C5 stream count: 2^20 streams create / save / load round trip (C++)
+    st, _ = sf.create_streams(sf.set_base_creator(), 1 << 20)
+    p = tmp_path / "c5.txt"
+    sf.save_streams_atomic(st, p)
+    back = sf.load_streams(p)
+    assert back == st
+
+
+def test_api_validation_without_device():
+    with pytest.raises(InvalidGridError):
+        sf.WorkGrid(0, 4)
+    with pytest.raises(InvalidGridError):
+        sf.WorkGrid(2, 3).require_paired_lanes()
+    assert sf.MatrixBuffer(2, 3).npad == 3
+    with pytest.raises(InvalidArgumentError):
+        sf.MatrixBuffer(2, 3, npad=2)
+    with pytest.raises(InvalidArgumentError):
+        sf.FillRequest(shape=(0, 3)).dims()
+    with pytest.raises(InvalidArgumentError):
+        sf.FillRequest(shape=(1, 2, 3)).dims()
+    with pytest.raises(InvalidArgumentError):
+        sf.FillRequest(shape=4, kind="poisson").dims()
+    with pytest.raises(InvalidRateError):
+        sf.FillRequest(shape=4, kind="exponential", rate=0.0).dims()
+    assert sf.FillRequest(shape=7).dims() == (1, 7, True)
+    assert sf.FillRequest(shape=(7,)).dims() == (1, 7, True)
+    streams = sf.create_streams(sf.set_base_creator(), 3)[0]
+    with pytest.raises(InsufficientStreamsError):
+        sf.run_grid(streams, sf.WorkGrid(2, 2), 2, 2, "uniform")
+    with pytest.raises(InvalidGridError):
+        sf.fill_normal(sf.create_streams(sf.set_base_creator(), 6)[0],
+                       sf.FillRequest(shape=(2, 2), grid=sf.WorkGrid(2, 3)))
+    with pytest.raises(InvalidArgumentError):
+        sf.ContingencyTable([[5]])
+    with pytest.raises(InvalidArgumentError):
+        sf.ContingencyTable([[1, -1], [0, 2]])
+    with pytest.raises(InvalidMarginsError):
+        sf.rcont2([3, 3], [2, 2], np.array([12345] * 6, np.int64))
+    month = np.ones((3, 3), np.int64)
+    with pytest.raises(InvalidArgumentError):
+        sf.fisher_sim(month, 0, sf.create_streams(sf.set_base_creator(), 16)[0],
+                      grid=sf.WorkGrid(4, 4))
+    with pytest.raises(InsufficientStreamsError):
+        sf.fisher_sim(month, 100, sf.create_streams(sf.set_base_creator(), 4)[0],
+                      grid=sf.WorkGrid(4, 4))
+    g = sf.WorkGrid(256, 64)
+    assert sim_num_for(10 ** 6, g) == 1015808
+    assert sim_num_for(10 ** 7, g) == 10010624
+    assert relaxed_threshold(-47955.0) > -47955.0
+
+
+def test_thresholds_match_reference(G, A):
+    assert sf.logfact_sum(A["month"]) == G["threshold_month"]
+    assert sf.logfact_sum(A["week"]) == G["threshold_week"]
+    assert sf.logfact_sum(np.array(G["T10"])) == G["threshold_T10"]
+    assert np.array_equal(log_factorial_table(int(A["month"].sum())), A["lf_month"])
+    t = ContingencyTable(A["month"])
+    assert t.row_margins.sum() == t.total == t.col_margins.sum()
+
+
+def test_element_plan_and_stream_index():
+    plan = sf.element_plan(sf.WorkGrid(2, 2), 3, 3)
+    assert plan[(0, 0)] == [(0, 0), (0, 2), (2, 0), (2, 2)]
+    grid = sf.WorkGrid(2, 2)
+    assert sf.stream_index("uniform", grid, 0, 1) == 2
+    assert sf.stream_index("normal", grid, 1, 0) == 2
+    with pytest.raises(InvalidArgumentError):
+        sf.stream_index("uniform", grid, 2, 0)
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_product_path_fails_loudly_without_gpu():
+    streams = sf.create_streams(sf.set_base_creator(), 4)[0]
+    with pytest.raises(DeviceError):
+        sf.fill_uniform(streams, sf.FillRequest(shape=8, grid=sf.WorkGrid(2, 2)))
+    with pytest.raises(DeviceError):
+        sf.fisher_sim([[1, 2], [3, 4]], 10, streams, grid=sf.WorkGrid(2, 2))
