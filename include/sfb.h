@@ -138,6 +138,10 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
 int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out);
 /* the device exp() port (glibc __exp FMA variant) evaluated on the host */
 double sfb_host_exp(double x);
+/* the device Box-Muller pair transform (box_muller.cuh) evaluated on the host
+ * for draws z1[k], z2[k] in [1, m1]: a = R cos(theta), b = R cos(theta - pi/2) */
+int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,
+                        double *b);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,7 @@ def lib():
         L.orc_skip.argtypes = [_i64p, ctypes.c_uint64]
         L.orc_create_streams.argtypes = [_i64p, ctypes.c_int64, _i64p, _i64p]
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_box_muller.argtypes = [_i64p, _i64p, ctypes.c_int64, _f64p, _f64p]
         _lib = L
     return _lib
 
@@ -155,3 +156,13 @@ def create_streams(seed, n):
     nxt = np.empty(6, np.int64)
     lib().orc_create_streams(_p(seed, _i64p), int(n), _p(rows, _i64p), _p(nxt, _i64p))
     return rows, tuple(int(x) for x in nxt)
+
+
+def box_muller(z1, z2):
+    """_kernels.py:147-152 on arbitrary draws (libm log/cos/sqrt)."""
+    z1 = _i64(z1)
+    z2 = _i64(z2)
+    a = np.empty(len(z1))
+    b = np.empty(len(z1))
+    lib().orc_box_muller(_p(z1, _i64p), _p(z2, _i64p), len(z1), _p(a, _f64p), _p(b, _f64p))
+    return a, b

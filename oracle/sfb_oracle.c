@@ -152,6 +152,20 @@ void orc_fill_normal(int64_t *cur, double *out_f64, float *out_f32,
     }
 }
 
+/* _kernels.py:147-152 for arbitrary draw pairs (z1, z2) in [1, m1]: the
+ * transform alone, used to measure the device port's accuracy at scale. */
+void orc_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,
+                    double *b) {
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < n; ++k) {
+        double u1 = (double)z1[k] * NORM;
+        double theta = (TWOPI * NORM) * (double)z2[k];
+        double radius = sqrt(-2.0 * log(u1));
+        a[k] = radius * cos(theta);
+        b[k] = radius * cos(theta - HALFPI);
+    }
+}
+
 /* One conditional-hypergeometric cell draw, _kernels.py:205-261 (shared with
  * rcont2_table, _kernels.py:322-375).  Consumes exactly one step. */
 static inline int64_t sample_cell(int64_t ia, int64_t idv, int64_t ie,

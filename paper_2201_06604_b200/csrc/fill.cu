@@ -30,12 +30,10 @@
 
 #include <algorithm>
 
+#include "box_muller.cuh"
 #include "sfb_internal.h"
 
 namespace sfb {
-
-constexpr double kTwoPiNorm = (2.0 * 3.141592653589793) / 2147483648.0;  // TWOPI*NORM, exact
-constexpr double kHalfPi = 0.5 * 3.141592653589793;                      // _kernels.py:22
 
 enum Kind { kUniform = 0, kExponential = 1, kInteger = 2 };
 
@@ -48,11 +46,16 @@ __device__ __forceinline__ int64_t owned(int64_t n, int64_t idx, int64_t g) {
     return idx < n ? (n - idx + g - 1) / g : 0;
 }
 
+// u = z * NORM (_kernels.py:70) from zm1 = z - 1: fma(zm1, 2^-31, 2^-31) is exact
+__device__ __forceinline__ double u01(uint32_t zm1) {
+    return __fma_rn((double)zm1, kNorm, kNorm);
+}
+
 template <int KIND>
-__device__ __forceinline__ double real_value(uint32_t z, double rate) {
-    const double u = (double)z * kNorm;  // _kernels.py:70, exact
+__device__ __forceinline__ double real_value(uint32_t zm1, double rate) {
+    const double u = u01(zm1);
     if (KIND == kUniform) return u;
-    return -log1p(-u) / rate;  // _kernels.py:74 (CUDA log1p: tolerance, not bit-exact)
+    return __ddiv_rn(-log1p(-u), rate);  // _kernels.py:74 (CUDA log1p: tolerance, not bit-exact)
 }
 
 // ---------------------------------------------------------------------------
@@ -77,12 +80,12 @@ __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict_
     skip(tab, s, (uint64_t)d0);
     int64_t rho = d0 / nc, q = d0 % nc;
     for (int64_t d = d0; d < d1; ++d) {
-        const uint32_t z = step(s);
+        const uint32_t zm1 = step_m1(s);
         const int64_t off = (i + g.g0 * rho) * g.npad + j + g.g1 * q;
         if (KIND == kInteger)
-            __stcs((long long *)out + off, (long long)z);
+            __stcs((long long *)out + off, (long long)zm1 + 1);
         else
-            __stcs((double *)out + off, real_value<KIND>(z, rate));
+            __stcs((double *)out + off, real_value<KIND>(zm1, rate));
         if (++q == nc) {
             q = 0;
             ++rho;
@@ -124,23 +127,24 @@ __global__ void __launch_bounds__(256) fill_uniform_fast(int64_t *__restrict__ c
 #pragma unroll 3
             for (int64_t q = 0; q < nb; ++q) {
                 longlong2 v;
-                v.x = step(sa);
-                v.y = step(sb);
+                v.x = (long long)step_m1(sa) + 1;
+                v.y = (long long)step_m1(sb) + 1;
                 __stcs(p + q * stride, v);
             }
-            if (na > nb) __stcs((long long *)out + rowoff + g.g1 * nb, (long long)step(sa));
+            if (na > nb)
+                __stcs((long long *)out + rowoff + g.g1 * nb, (long long)step_m1(sa) + 1);
         } else {
             double2 *p = (double2 *)((double *)out + rowoff);
             const int64_t stride = g.g1 / 2;
 #pragma unroll 3
             for (int64_t q = 0; q < nb; ++q) {
                 double2 v;
-                v.x = real_value<KIND>(step(sa), rate);
-                v.y = real_value<KIND>(step(sb), rate);
+                v.x = real_value<KIND>(step_m1(sa), rate);
+                v.y = real_value<KIND>(step_m1(sb), rate);
                 __stcs(p + q * stride, v);
             }
             if (na > nb)
-                __stcs((double *)out + rowoff + g.g1 * nb, real_value<KIND>(step(sa), rate));
+                __stcs((double *)out + rowoff + g.g1 * nb, real_value<KIND>(step_m1(sa), rate));
         }
     }
     if (rho1 == nr) {
@@ -150,22 +154,34 @@ __global__ void __launch_bounds__(256) fill_uniform_fast(int64_t *__restrict__ c
 }
 
 // ---------------------------------------------------------------------------
-// Box-Muller pair (_kernels.py:145-152), computed in fp64:
-//   u1 = z1*NORM, theta = (2 pi NORM)*z2, R = sqrt(-2 log u1),
-//   a = R cos(theta), b = R cos(theta - pi/2)
-// CUDA's log/cos are within 1-2 ulp of glibc's (tolerance stated in
-// DESIGN.md and tests); the float32 variant rounds the fp64 value once.
-__device__ __forceinline__ void box_muller(uint32_t z1, uint32_t z2, double &a, double &b) {
-    const double u1 = (double)z1 * kNorm;
-    const double theta = kTwoPiNorm * (double)z2;
-    const double radius = sqrt(-2.0 * log(u1));
-    a = radius * cos(theta);
-    b = radius * cos(theta - kHalfPi);
-}
+// Box-Muller fills (_kernels.py:108-166).  The transform is box_muller_pair()
+// (box_muller.cuh): fp64 throughout, float32 output rounds the fp64 value once.
 
 template <typename T>
 __device__ __forceinline__ void put(T *out, int64_t off, double v) {
     __stcs(out + off, (T)v);
+}
+
+__device__ __forceinline__ void put4(float *p, double a, double b, double c, double d) {
+    __stcs((float4 *)p, make_float4((float)a, (float)b, (float)c, (float)d));
+}
+__device__ __forceinline__ void put4(double *p, double a, double b, double c, double d) {
+    __stcs((double2 *)p, make_double2(a, b));
+    __stcs((double2 *)p + 1, make_double2(c, d));
+}
+__device__ __forceinline__ void put2(float *p, double a, double b) {
+    __stcs((float2 *)p, make_float2((float)a, (float)b));
+}
+__device__ __forceinline__ void put2(double *p, double a, double b) {
+    __stcs((double2 *)p, make_double2(a, b));
+}
+
+// the 128-bucket log table of box_muller.cuh, staged in shared memory
+__device__ __forceinline__ const uint64_t *stage_log_table(uint64_t *smem) {
+    static const uint64_t kLogTab[3 * 128] = SFB_BM_LOG_TABLE_INIT;
+    for (int t = threadIdx.x; t < 3 * 128; t += blockDim.x) smem[t] = kLogTab[t];
+    __syncthreads();
+    return smem;
 }
 
 // normal, generic layout: unit = (pair, chunk of pair-iterations)
@@ -175,6 +191,8 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
                                                            int64_t pair_lo, int64_t nloc,
                                                            int64_t chunk, int64_t nunits,
                                                            const __grid_constant__ Pow2Table tab) {
+    __shared__ uint64_t logtab_s[3 * 128];
+    const uint64_t *logtab = stage_log_table(logtab_s);
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t p = pair_lo + u % nloc;
@@ -193,9 +211,10 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
     skip(tab, sb, (uint64_t)d0);
     int64_t rho = d0 / niter, q = d0 % niter;
     for (int64_t d = d0; d < d1; ++d) {
-        const uint32_t z1 = step(sa), z2 = step(sb);
         double a, b;
-        box_muller(z1, z2, a, b);
+        const uint32_t z1 = step_m1(sa);
+        const uint32_t z2 = step_m1(sb);
+        box_muller_pair(z1, z2, logtab, a, b);
         const int64_t ca = j0 + g.g1 * q;
         const int64_t off = (i + g.g0 * rho) * g.npad + ca;
         put(out, off, a);
@@ -211,67 +230,73 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
     }
 }
 
-template <typename T>
-struct Vec2;
-template <>
-struct Vec2<double> {
-    using type = double2;
-};
-template <>
-struct Vec2<float> {
-    using type = float2;
-};
-
-// normal, pair fast path (npad even): unit = (chunk, grid row i, pair jp)
-template <typename T>
+// normal, fast path: unit = (chunk, grid row i, group of PAIRS adjacent pairs)
+//   PAIRS == 1: npad even; handles a partner past ncol on the last trip.
+//   PAIRS == 2: g1 % 4 == 0, ncol % 4 == 0, npad % 4 == 0 -> both pairs of a
+//               thread have the same trip count and always-valid partners; one
+//               16-byte store (float32) per trip.
+template <typename T, int PAIRS>
 __global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cur,
                                                         T *__restrict__ out, Geom g,
                                                         int64_t i_lo, int64_t nrows_grid,
                                                         int64_t rows_per_chunk, int64_t nunits,
                                                         const __grid_constant__ Pow2Table tab) {
-    using V = typename Vec2<T>::type;
+    __shared__ uint64_t logtab_s[3 * 128];
+    const uint64_t *logtab = stage_log_table(logtab_s);
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
-    const int64_t half = g.g1 / 2;
-    const int64_t jp = u % half;
-    const int64_t ic = u / half;
+    const int64_t groups = g.g1 / (2 * PAIRS);
+    const int64_t jq = u % groups;
+    const int64_t ic = u / groups;
     const int64_t i = i_lo + ic % nrows_grid, c = ic / nrows_grid;
-    const int64_t j0 = 2 * jp;
+    const int64_t j0 = 2 * PAIRS * jq;
     const int64_t nr = owned(g.nrow, i, g.g0);
     const int64_t rho0 = c * rows_per_chunk;
     if (rho0 >= nr) return;
     const int64_t rho1 = min(rho0 + rows_per_chunk, nr);
     const int64_t niter = owned(g.ncol, j0, g.g1);
     const int64_t s0 = i * g.g1 + j0;
-    Mrg sa = load_state(cur + 6 * s0), sb = load_state(cur + 6 * (s0 + 1));
-    if (rho0) {
-        skip(tab, sa, (uint64_t)(rho0 * niter));
-        skip(tab, sb, (uint64_t)(rho0 * niter));
+    Mrg st[2 * PAIRS];
+#pragma unroll
+    for (int k = 0; k < 2 * PAIRS; ++k) {
+        st[k] = load_state(cur + 6 * (s0 + k));
+        if (rho0) skip(tab, st[k], (uint64_t)(rho0 * niter));
     }
-    // the last trip of a row may have its partner column past ncol
-    const bool partner_last = j0 + 1 + g.g1 * (niter - 1) < g.ncol;
-    const int64_t nfull = partner_last ? niter : niter - 1;
-    for (int64_t rho = rho0; rho < rho1; ++rho) {
-        const int64_t rowoff = (i + g.g0 * rho) * g.npad + j0;
-        V *p = (V *)(out + rowoff);
-#pragma unroll 3
-        for (int64_t q = 0; q < nfull; ++q) {
-            double a, b;
-            box_muller(step(sa), step(sb), a, b);
-            V v;
-            v.x = (T)a;
-            v.y = (T)b;
-            __stcs(p + q * half, v);
+    if (PAIRS == 2) {
+        for (int64_t rho = rho0; rho < rho1; ++rho) {
+            T *p = out + (i + g.g0 * rho) * g.npad + j0;
+            for (int64_t q = 0; q < niter; ++q) {
+                double a0, b0, a1, b1;
+                const uint32_t z0 = step_m1(st[0]), z1 = step_m1(st[1]);
+                const uint32_t z2 = step_m1(st[2]), z3 = step_m1(st[3]);
+                box_muller_pair(z0, z1, logtab, a0, b0);
+                box_muller_pair(z2, z3, logtab, a1, b1);
+                put4(p + g.g1 * q, a0, b0, a1, b1);
+            }
         }
-        if (nfull < niter) {
-            double a, b;
-            box_muller(step(sa), step(sb), a, b);
-            put(out, rowoff + g.g1 * nfull, a);
+    } else {
+        // the last trip of a row may have its partner column past ncol
+        const bool partner_last = j0 + 1 + g.g1 * (niter - 1) < g.ncol;
+        const int64_t nfull = partner_last ? niter : niter - 1;
+        for (int64_t rho = rho0; rho < rho1; ++rho) {
+            T *p = out + (i + g.g0 * rho) * g.npad + j0;
+            for (int64_t q = 0; q < nfull; ++q) {
+                double a, b;
+                const uint32_t z1 = step_m1(st[0]), z2 = step_m1(st[1]);
+                box_muller_pair(z1, z2, logtab, a, b);
+                put2(p + g.g1 * q, a, b);
+            }
+            if (nfull < niter) {
+                double a, b;
+                const uint32_t z1 = step_m1(st[0]), z2 = step_m1(st[1]);
+                box_muller_pair(z1, z2, logtab, a, b);
+                put(p, g.g1 * nfull, a);
+            }
         }
     }
     if (rho1 == nr) {
-        store_state(cur + 6 * s0, sa);
-        store_state(cur + 6 * (s0 + 1), sb);
+#pragma unroll
+        for (int k = 0; k < 2 * PAIRS; ++k) store_state(cur + 6 * (s0 + k), st[k]);
     }
 }
 
@@ -364,8 +389,9 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
     if (fast) {
         const int64_t i_lo = pair_lo / half;
         const int64_t nrows_grid = (pair_hi - pair_lo) / half;
+        const bool two = g.g1 % 4 == 0 && g.ncol % 4 == 0 && g.npad % 4 == 0;
         const int64_t rows = ceil_div(g.nrow, g.g0);
-        const int64_t base = nrows_grid * half;
+        const int64_t base = nrows_grid * half / (two ? 2 : 1);
         const int64_t cols = ceil_div(g.ncol, g.g1);
         const int64_t min_rows = std::max<int64_t>(1, kMinChunkDraws / std::max<int64_t>(1, cols));
         int64_t nchunks = std::max<int64_t>(1, std::min(ceil_div(kTargetUnits, base),
@@ -373,8 +399,13 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
         const int64_t rpc = ceil_div(rows, nchunks);
         nchunks = ceil_div(rows, rpc);
         const int64_t nunits = base * nchunks;
-        fill_normal_fast<T><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
-            cur, out, g, i_lo, nrows_grid, rpc, nunits, tab);
+        const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
+        if (two)
+            fill_normal_fast<T, 2><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo, nrows_grid,
+                                                                 rpc, nunits, tab);
+        else
+            fill_normal_fast<T, 1><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo, nrows_grid,
+                                                                 rpc, nunits, tab);
         return launch_check("fill_normal_fast");
     }
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);

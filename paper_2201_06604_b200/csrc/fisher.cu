@@ -59,8 +59,8 @@ struct FisherArgs {
 template <typename LF>
 __device__ __forceinline__ int sample_cell(int ia, int idv, int ie, int ib, int ic, int ii,
                                            const LF &lf, const uint64_t *exptab, Mrg &s) {
-    const uint32_t z = step(s);  // _kernels.py:211
-    const double u = (double)z * kNorm;
+    const uint32_t zm1 = step_m1(s);  // _kernels.py:211-212: u = z * NORM, exact
+    const double u = __fma_rn((double)zm1, kNorm, kNorm);
     int lo = ia + idv - ie;
     if (lo < 0) lo = 0;
     const int hi = ia < idv ? ia : idv;

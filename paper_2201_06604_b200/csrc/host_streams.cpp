@@ -19,6 +19,7 @@
 #include <mutex>
 #include <string>
 
+#include "box_muller.cuh"
 #include "exp_glibc.cuh"
 #include "sfb_internal.h"
 
@@ -432,5 +433,16 @@ int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out)
 }
 
 double sfb_host_exp(double x) { return glibc_exp(x, kExpTable); }
+
+int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,
+                        double *b) {
+    static const uint64_t kLogTab[3 * 128] = SFB_BM_LOG_TABLE_INIT;
+    for (int64_t k = 0; k < n; ++k) {
+        if (z1[k] < 1 || z1[k] > (int64_t)kM1 || z2[k] < 1 || z2[k] > (int64_t)kM1)
+            return fail(SFB_E_INVALID_ARGUMENT, "draws must lie in [1, m1]");
+        box_muller_pair((uint32_t)(z1[k] - 1), (uint32_t)(z2[k] - 1), kLogTab, a[k], b[k]);
+    }
+    return SFB_OK;
+}
 
 }  // extern "C"

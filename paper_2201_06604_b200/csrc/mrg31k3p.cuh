@@ -6,14 +6,10 @@
 //   y2 = (2^15*b0 + (2^15+1)*b2) mod m2, shift (b0,b1,b2) <- (y2,b0,b1)
 //   z  = y1 - y2, z <= 0 => z += m1          (z in [1, m1])
 //
-// B200 formulation: everything in uint32 registers, no 64-bit multiply.
-//   component 1: for x < m1 = 2^31-1, 2^k x mod m1 is the 31-bit rotation
-//     rot31(x, k), which is again < m1; so y1 = rot22(a1) + rot7(a2) + a2 with
-//     two conditional subtractions (each sum stays < 2^32).
-//   component 2: with t = b0 + b2 (< 2^32), 2^15 t = (t>>16) 2^31 + (t&0xffff) 2^15
-//     and 2^31 == 21069 (mod m2), so 2^15 t == (t>>16)*21069 + ((t&0xffff)<<15)
-//     (< 2^32), one conditional subtraction, then + b2 and one more.
-// Conditional subtraction is min(v, v - m) on unsigned values (v < 2m).
+// B200 formulation (step_m1 below): uint32 state registers, one 32x32->64
+// IMAD.WIDE per component product, a single Mersenne-style fold per component
+// and one conditional subtraction each; csub(v, m) = min(v, v - m) on
+// unsigned values (v < 2m) compiles to one VIADDMNMX on sm_100a.
 // Verified against the int64 oracle step on random and extreme states by the
 // CPU test tests/test_host_lib.py (through sfb_host_step_u32).
 #pragma once
@@ -45,23 +41,29 @@ struct Mrg {
     uint32_t a0, a1, a2, b0, b1, b2;
 };
 
-// one MRG31k3p step (_kernels.py:33-47); returns z in [1, m1]
-SFB_HD uint32_t step(Mrg &s) {
-    const uint32_t r22 = ((s.a1 << 22) & kM1) | (s.a1 >> 9);
-    const uint32_t r7 = ((s.a2 << 7) & kM1) | (s.a2 >> 24);
-    uint32_t y1 = csub(r22 + r7, kM1);
-    y1 = csub(y1 + s.a2, kM1);
+// one MRG31k3p step (_kernels.py:33-47); returns z - 1 in [0, m1 - 1]
+// (callers fold the +1 into their next operation, e.g. u = fma(z-1, 2^-31, 2^-31)).
+//   component 1: p = 2^22 a1 + 129 a2 < 2^54 (two IMAD.WIDE), and since
+//     2^31 == 1 (mod m1), p == (p & m1) + (p >> 31) < 2m1: one csub.
+//   component 2: p = 2^15 (b0 + b2) + b2 < 2^48, 2^31 == 21069 (mod m2):
+//     p == (p >> 31) * 21069 + (p & m1) < 2m2: one csub.
+//   z - 1 = y1 - y2 - 1 (+ m1 if y1 <= y2) = csub(y1 - y2 + m1 - 1, m1).
+SFB_HD uint32_t step_m1(Mrg &s) {
+    const uint64_t p1 = (uint64_t)s.a1 * 4194304u + (uint64_t)s.a2 * 129u;
+    const uint32_t y1 = csub(((uint32_t)p1 & kM1) + (uint32_t)(p1 >> 31), kM1);
     s.a2 = s.a1;
     s.a1 = s.a0;
     s.a0 = y1;
-    const uint32_t t = s.b0 + s.b2;
-    uint32_t y2 = csub((t >> 16) * 21069u + ((t & 0xffffu) << 15), kM2);
-    y2 = csub(y2 + s.b2, kM2);
+    const uint64_t p2 = ((uint64_t)(s.b0 + s.b2) << 15) + s.b2;
+    const uint32_t y2 = csub((uint32_t)(p2 >> 31) * 21069u + ((uint32_t)p2 & kM1), kM2);
     s.b2 = s.b1;
     s.b1 = s.b0;
     s.b0 = y2;
-    return y1 > y2 ? y1 - y2 : y1 - y2 + kM1;
+    return csub(y1 - y2 + (kM1 - 1u), kM1);
 }
+
+// one MRG31k3p step (_kernels.py:33-47); returns z in [1, m1]
+SFB_HD uint32_t step(Mrg &s) { return step_m1(s) + 1u; }
 
 SFB_HD Mrg load_state(const int64_t *row) {
     Mrg s;

@@ -326,3 +326,51 @@ def test_product_path_fails_loudly_without_gpu():
         sf.fill_uniform(streams, sf.FillRequest(shape=8, grid=sf.WorkGrid(2, 2)))
     with pytest.raises(DeviceError):
         sf.fisher_sim([[1, 2], [3, 4]], 10, streams, grid=sf.WorkGrid(2, 2))
+
+
+def _host_bm(z1, z2):
+    z1 = np.ascontiguousarray(z1, np.int64)
+    z2 = np.ascontiguousarray(z2, np.int64)
+    a = np.empty(len(z1))
+    b = np.empty(len(z1))
+    _lib.check(_lib.lib().sfb_host_box_muller(_lib.ptr(z1), _lib.ptr(z2), len(z1),
+                                              _lib.ptr(a, _lib._f64p), _lib.ptr(b, _lib._f64p)))
+    return a, b
+
+
+def _bm_draws(n, seed=11):
+    rng = np.random.default_rng(seed)
+    z1 = rng.integers(1, sf.M1 + 1, n)
+    z2 = rng.integers(1, sf.M1 + 1, n)
+    # edges: u1 -> 0 and -> 1, powers of two, theta at/near multiples of pi/2
+    e1 = [1, 2, 3, 2 ** 30, 2 ** 30 + 1, 2 ** 31 - 2 ** 24, sf.M1 - 1, sf.M1]
+    e2 = [1, 2, 2 ** 29 - 1, 2 ** 29, 2 ** 29 + 1, 2 ** 30 - 1, 2 ** 30, 2 ** 30 + 1,
+          3 * 2 ** 29 - 1, 3 * 2 ** 29, 3 * 2 ** 29 + 1, 2 ** 28, 2 ** 28 + 1, sf.M1 - 1, sf.M1,
+          2 ** 31 - 2 ** 28, 2 ** 31 - 2 ** 28 + 1]
+    z1 = np.concatenate([z1, np.repeat(e1, len(e2)), rng.integers(sf.M1 - 2 ** 20, sf.M1 + 1,
+                                                                   n // 8)])
+    z2 = np.concatenate([z2, np.tile(e2, len(e1)), rng.integers(1, sf.M1 + 1, n // 8)])
+    near = np.concatenate([k * 2 ** 29 + np.arange(-50, 51) for k in (1, 2, 3, 4)])
+    near = near[(near >= 1) & (near <= sf.M1)]
+    z1 = np.concatenate([z1, rng.integers(1, sf.M1 + 1, len(near))])
+    z2 = np.concatenate([z2, near])
+    return z1, z2
+
+
+def test_box_muller_port_against_libm():
+    """The device Box-Muller (box_muller.cuh), run on the host, against the
+    reference formula on glibc (oracle).  Contract:
+      f64: |port - ref| <= 4 ulp(ref) or <= 2^-60 absolute;
+      f32: |f32(port) - f32(ref)| <= 1 ulp_f32, equal on >= 99.999 %."""
+    z1, z2 = _bm_draws(2_000_000)
+    a, b = _host_bm(z1, z2)
+    ra, rb = orc.box_muller(z1, z2)
+    for got, ref in ((a, ra), (b, rb)):
+        err = np.abs(got - ref)
+        ok = (err <= 4 * np.spacing(np.abs(ref))) | (err <= 2.0 ** -60)
+        assert ok.all(), (got[~ok][:4], ref[~ok][:4], z1[~ok][:4], z2[~ok][:4])
+        g32, r32 = got.astype(np.float32), ref.astype(np.float32)
+        eq = g32 == r32
+        d = np.abs(g32.astype(np.float64) - r32.astype(np.float64))
+        assert (d <= np.spacing(np.abs(r32)).astype(np.float64)).all()
+        assert eq.mean() >= 0.99999, eq.mean()
