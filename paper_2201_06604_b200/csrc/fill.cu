@@ -58,6 +58,26 @@ __device__ __forceinline__ double real_value(uint32_t zm1, double rate) {
     return __ddiv_rn(-log1p(-u), rate);  // _kernels.py:74 (CUDA log1p: tolerance, not bit-exact)
 }
 
+// one 16-byte streaming store of a column pair / one 8-byte store
+template <int KIND>
+__device__ __forceinline__ void put_pair(void *out, int64_t off, uint32_t za, uint32_t zb,
+                                         double rate) {
+    if (KIND == kInteger)
+        __stcs((longlong2 *)((long long *)out + off),
+               make_longlong2((long long)za + 1, (long long)zb + 1));
+    else
+        __stcs((double2 *)((double *)out + off),
+               make_double2(real_value<KIND>(za, rate), real_value<KIND>(zb, rate)));
+}
+
+template <int KIND>
+__device__ __forceinline__ void put_one(void *out, int64_t off, uint32_t za, double rate) {
+    if (KIND == kInteger)
+        __stcs((long long *)out + off, (long long)za + 1);
+    else
+        __stcs((double *)out + off, real_value<KIND>(za, rate));
+}
+
 // ---------------------------------------------------------------------------
 // uniform kinds, generic layout
 template <int KIND>
@@ -121,31 +141,20 @@ __global__ void __launch_bounds__(256) fill_uniform_fast(int64_t *__restrict__ c
     }
     for (int64_t rho = rho0; rho < rho1; ++rho) {
         const int64_t rowoff = (i + g.g0 * rho) * g.npad + j;
-        if (KIND == kInteger) {
-            longlong2 *p = (longlong2 *)((long long *)out + rowoff);
-            const int64_t stride = g.g1 / 2;
-#pragma unroll 3
-            for (int64_t q = 0; q < nb; ++q) {
-                longlong2 v;
-                v.x = (long long)step_m1(sa) + 1;
-                v.y = (long long)step_m1(sb) + 1;
-                __stcs(p + q * stride, v);
-            }
-            if (na > nb)
-                __stcs((long long *)out + rowoff + g.g1 * nb, (long long)step_m1(sa) + 1);
-        } else {
-            double2 *p = (double2 *)((double *)out + rowoff);
-            const int64_t stride = g.g1 / 2;
-#pragma unroll 3
-            for (int64_t q = 0; q < nb; ++q) {
-                double2 v;
-                v.x = real_value<KIND>(step_m1(sa), rate);
-                v.y = real_value<KIND>(step_m1(sb), rate);
-                __stcs(p + q * stride, v);
-            }
-            if (na > nb)
-                __stcs((double *)out + rowoff + g.g1 * nb, real_value<KIND>(step_m1(sa), rate));
+        int64_t q = 0;
+        for (; q + 3 <= nb; q += 3) {  // step3: no shift-register moves
+            uint32_t a0, a1, a2, b0, b1, b2;
+            step3(sa, a0, a1, a2);
+            step3(sb, b0, b1, b2);
+            put_pair<KIND>(out, rowoff + g.g1 * q, a0, b0, rate);
+            put_pair<KIND>(out, rowoff + g.g1 * (q + 1), a1, b1, rate);
+            put_pair<KIND>(out, rowoff + g.g1 * (q + 2), a2, b2, rate);
         }
+        for (; q < nb; ++q) {
+            const uint32_t za = step_m1(sa), zb = step_m1(sb);
+            put_pair<KIND>(out, rowoff + g.g1 * q, za, zb, rate);
+        }
+        if (na > nb) put_one<KIND>(out, rowoff + g.g1 * nb, step_m1(sa), rate);
     }
     if (rho1 == nr) {
         store_state(cur + 6 * wa, sa);
@@ -177,9 +186,16 @@ __device__ __forceinline__ void put2(double *p, double a, double b) {
 }
 
 // the 128-bucket log table of box_muller.cuh, staged in shared memory
-__device__ __forceinline__ const uint64_t *stage_log_table(uint64_t *smem) {
-    static const uint64_t kLogTab[3 * 128] = SFB_BM_LOG_TABLE_INIT;
-    for (int t = threadIdx.x; t < 3 * 128; t += blockDim.x) smem[t] = kLogTab[t];
+constexpr int kBmLogWords = 3 * SFB_BM_LOG_N;
+constexpr int kBmTabWords = kBmLogWords + 3 * (SFB_BM_TRIG_N + 1);
+
+// log table then trig table (box_muller.cuh), staged in shared memory (36.6 KB)
+__device__ __forceinline__ const uint64_t *stage_bm_tables(uint64_t *smem) {
+    static const uint64_t kLogTab[kBmLogWords] = SFB_BM_LOG_TABLE_INIT;
+    static const uint64_t kTrigTab[kBmTabWords - kBmLogWords] = SFB_BM_TRIG_TABLE_INIT;
+    for (int t = threadIdx.x; t < kBmLogWords; t += blockDim.x) smem[t] = kLogTab[t];
+    for (int t = threadIdx.x; t < kBmTabWords - kBmLogWords; t += blockDim.x)
+        smem[kBmLogWords + t] = kTrigTab[t];
     __syncthreads();
     return smem;
 }
@@ -191,8 +207,9 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
                                                            int64_t pair_lo, int64_t nloc,
                                                            int64_t chunk, int64_t nunits,
                                                            const __grid_constant__ Pow2Table tab) {
-    __shared__ uint64_t logtab_s[3 * 128];
-    const uint64_t *logtab = stage_log_table(logtab_s);
+    __shared__ uint64_t bmtab_s[kBmTabWords];
+    const uint64_t *logtab = stage_bm_tables(bmtab_s);
+    const uint64_t *trigtab = logtab + kBmLogWords;
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t p = pair_lo + u % nloc;
@@ -214,7 +231,7 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
         double a, b;
         const uint32_t z1 = step_m1(sa);
         const uint32_t z2 = step_m1(sb);
-        box_muller_pair(z1, z2, logtab, a, b);
+        box_muller_pair(z1, z2, logtab, trigtab, a, b);
         const int64_t ca = j0 + g.g1 * q;
         const int64_t off = (i + g.g0 * rho) * g.npad + ca;
         put(out, off, a);
@@ -241,8 +258,9 @@ __global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cu
                                                         int64_t i_lo, int64_t nrows_grid,
                                                         int64_t rows_per_chunk, int64_t nunits,
                                                         const __grid_constant__ Pow2Table tab) {
-    __shared__ uint64_t logtab_s[3 * 128];
-    const uint64_t *logtab = stage_log_table(logtab_s);
+    __shared__ uint64_t bmtab_s[kBmTabWords];
+    const uint64_t *logtab = stage_bm_tables(bmtab_s);
+    const uint64_t *trigtab = logtab + kBmLogWords;
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t groups = g.g1 / (2 * PAIRS);
@@ -265,12 +283,25 @@ __global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cu
     if (PAIRS == 2) {
         for (int64_t rho = rho0; rho < rho1; ++rho) {
             T *p = out + (i + g.g0 * rho) * g.npad + j0;
-            for (int64_t q = 0; q < niter; ++q) {
+            int64_t q = 0;
+            for (; q + 3 <= niter; q += 3) {  // step3: no shift-register moves
+                uint32_t z[4][3];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) step3(st[k], z[k][0], z[k][1], z[k][2]);
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    double a0, b0, a1, b1;
+                    box_muller_pair(z[0][t], z[1][t], logtab, trigtab, a0, b0);
+                    box_muller_pair(z[2][t], z[3][t], logtab, trigtab, a1, b1);
+                    put4(p + g.g1 * (q + t), a0, b0, a1, b1);
+                }
+            }
+            for (; q < niter; ++q) {
                 double a0, b0, a1, b1;
                 const uint32_t z0 = step_m1(st[0]), z1 = step_m1(st[1]);
                 const uint32_t z2 = step_m1(st[2]), z3 = step_m1(st[3]);
-                box_muller_pair(z0, z1, logtab, a0, b0);
-                box_muller_pair(z2, z3, logtab, a1, b1);
+                box_muller_pair(z0, z1, logtab, trigtab, a0, b0);
+                box_muller_pair(z2, z3, logtab, trigtab, a1, b1);
                 put4(p + g.g1 * q, a0, b0, a1, b1);
             }
         }
@@ -280,16 +311,29 @@ __global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cu
         const int64_t nfull = partner_last ? niter : niter - 1;
         for (int64_t rho = rho0; rho < rho1; ++rho) {
             T *p = out + (i + g.g0 * rho) * g.npad + j0;
-            for (int64_t q = 0; q < nfull; ++q) {
+            int64_t q = 0;
+            for (; q + 3 <= nfull; q += 3) {
+                uint32_t x0, x1, x2, y0, y1, y2;
+                step3(st[0], x0, x1, x2);
+                step3(st[1], y0, y1, y2);
+                double a, b;
+                box_muller_pair(x0, y0, logtab, trigtab, a, b);
+                put2(p + g.g1 * q, a, b);
+                box_muller_pair(x1, y1, logtab, trigtab, a, b);
+                put2(p + g.g1 * (q + 1), a, b);
+                box_muller_pair(x2, y2, logtab, trigtab, a, b);
+                put2(p + g.g1 * (q + 2), a, b);
+            }
+            for (; q < nfull; ++q) {
                 double a, b;
                 const uint32_t z1 = step_m1(st[0]), z2 = step_m1(st[1]);
-                box_muller_pair(z1, z2, logtab, a, b);
+                box_muller_pair(z1, z2, logtab, trigtab, a, b);
                 put2(p + g.g1 * q, a, b);
             }
             if (nfull < niter) {
                 double a, b;
                 const uint32_t z1 = step_m1(st[0]), z2 = step_m1(st[1]);
-                box_muller_pair(z1, z2, logtab, a, b);
+                box_muller_pair(z1, z2, logtab, trigtab, a, b);
                 put(p, g.g1 * nfull, a);
             }
         }

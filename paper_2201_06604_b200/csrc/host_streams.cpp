@@ -423,7 +423,17 @@ int sfb_parse_streams(const char *text, int64_t len, int64_t *current, int64_t *
 int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out) {
     for (int64_t w = 0; w < n; ++w) {
         Mrg s = load_state(states + 6 * w);
-        for (int64_t t = 0; t < steps; ++t) {
+        int64_t t = 0;
+        for (; t + 3 <= steps; t += 3) {  // the rotating-slot form used by the kernels
+            uint32_t z0, z1, z2;
+            step3(s, z0, z1, z2);
+            if (z_out) {
+                z_out[w * steps + t] = z0 + 1;
+                z_out[w * steps + t + 1] = z1 + 1;
+                z_out[w * steps + t + 2] = z2 + 1;
+            }
+        }
+        for (; t < steps; ++t) {
             uint32_t z = step(s);
             if (z_out) z_out[w * steps + t] = z;
         }
@@ -436,11 +446,13 @@ double sfb_host_exp(double x) { return glibc_exp(x, kExpTable); }
 
 int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,
                         double *b) {
-    static const uint64_t kLogTab[3 * 128] = SFB_BM_LOG_TABLE_INIT;
+    static const uint64_t kLogTab[3 * SFB_BM_LOG_N] = SFB_BM_LOG_TABLE_INIT;
+    static const uint64_t kTrigTab[3 * (SFB_BM_TRIG_N + 1)] = SFB_BM_TRIG_TABLE_INIT;
     for (int64_t k = 0; k < n; ++k) {
         if (z1[k] < 1 || z1[k] > (int64_t)kM1 || z2[k] < 1 || z2[k] > (int64_t)kM1)
             return fail(SFB_E_INVALID_ARGUMENT, "draws must lie in [1, m1]");
-        box_muller_pair((uint32_t)(z1[k] - 1), (uint32_t)(z2[k] - 1), kLogTab, a[k], b[k]);
+        box_muller_pair((uint32_t)(z1[k] - 1), (uint32_t)(z2[k] - 1), kLogTab, kTrigTab,
+                        a[k], b[k]);
     }
     return SFB_OK;
 }

@@ -45,21 +45,43 @@ struct Mrg {
 // (callers fold the +1 into their next operation, e.g. u = fma(z-1, 2^-31, 2^-31)).
 //   component 1: p = 2^22 a1 + 129 a2 < 2^54 (two IMAD.WIDE), and since
 //     2^31 == 1 (mod m1), p == (p & m1) + (p >> 31) < 2m1: one csub.
-//   component 2: p = 2^15 (b0 + b2) + b2 < 2^48, 2^31 == 21069 (mod m2):
-//     p == (p >> 31) * 21069 + (p & m1) < 2m2: one csub.
-//   z - 1 = y1 - y2 - 1 (+ m1 if y1 <= y2) = csub(y1 - y2 + m1 - 1, m1).
-SFB_HD uint32_t step_m1(Mrg &s) {
-    const uint64_t p1 = (uint64_t)s.a1 * 4194304u + (uint64_t)s.a2 * 129u;
+//   component 2: p = 2^15 b0 + (2^15+1) b2 < 2^48 (two IMAD.WIDE),
+//     2^31 == 21069 (mod m2): p == (p >> 31) * 21069 + (p & m1) < 2m2: one csub.
+//   z - 1 = y1 - y2 - 1 (+ m1 if y1 <= y2) = min(y1 - y2 - 1 + m1, y1 - y2 - 1).
+// step_core computes the new words from the lag values and writes them into
+// the slots of the dropped (oldest) words; step3 runs three steps with the
+// roles of the three slots rotating statically, so a loop over step3 needs no
+// register moves for the shift register.
+SFB_HD uint32_t step_core(uint32_t a1, uint32_t a2, uint32_t b0, uint32_t b2, uint32_t &a_out,
+                          uint32_t &b_out) {
+    const uint64_t p1 = (uint64_t)a1 * 4194304u + (uint64_t)a2 * 129u;
     const uint32_t y1 = csub(((uint32_t)p1 & kM1) + (uint32_t)(p1 >> 31), kM1);
+    const uint64_t p2 = (uint64_t)b0 * 32768u + (uint64_t)b2 * 32769u;
+    const uint32_t y2 = csub((uint32_t)(p2 >> 31) * 21069u + ((uint32_t)p2 & kM1), kM2);
+    a_out = y1;
+    b_out = y2;
+    const uint32_t dm1 = y1 - y2 - 1u;  // IADD3 + VIADDMNMX
+    return umin32(dm1 + kM1, dm1);
+}
+
+SFB_HD uint32_t step_m1(Mrg &s) {
+    uint32_t y1, y2;
+    const uint32_t zm1 = step_core(s.a1, s.a2, s.b0, s.b2, y1, y2);
     s.a2 = s.a1;
     s.a1 = s.a0;
     s.a0 = y1;
-    const uint64_t p2 = ((uint64_t)(s.b0 + s.b2) << 15) + s.b2;
-    const uint32_t y2 = csub((uint32_t)(p2 >> 31) * 21069u + ((uint32_t)p2 & kM1), kM2);
     s.b2 = s.b1;
     s.b1 = s.b0;
     s.b0 = y2;
-    return csub(y1 - y2 + (kM1 - 1u), kM1);
+    return zm1;
+}
+
+// three consecutive steps (z - 1 outputs in order); s ends in canonical order
+SFB_HD void step3(Mrg &s, uint32_t &z0, uint32_t &z1, uint32_t &z2) {
+    // slots (A0,A1,A2)=(a0,a1,a2), (B0,B1,B2)=(b0,b1,b2)
+    z0 = step_core(s.a1, s.a2, s.b0, s.b2, s.a2, s.b2);  // newest in A2/B2
+    z1 = step_core(s.a0, s.a1, s.b2, s.b1, s.a1, s.b1);  // newest in A1/B1
+    z2 = step_core(s.a2, s.a0, s.b1, s.b0, s.a0, s.b0);  // newest in A0/B0
 }
 
 // one MRG31k3p step (_kernels.py:33-47); returns z in [1, m1]
