@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
 //   PAIRS == 2: g1 % 4 == 0, ncol % 4 == 0, npad % 4 == 0 -> both pairs of a
 //               thread have the same trip count and always-valid partners; one
 //               16-byte store (float32) per trip.
-template <typename T, int PAIRS>
-__global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cur,
+template <typename T, int PAIRS, int MINB>
+__global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restrict__ cur,
                                                         T *__restrict__ out, Geom g,
                                                         int64_t i_lo, int64_t nrows_grid,
                                                         int64_t rows_per_chunk, int64_t nunits,
@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(256) fill_normal_fast(int64_t *__restrict__ cu
 // host-side launch planning
 
 constexpr int kThreads = 256;
+constexpr int kNormalVariantDefault = 0;
 // enough units to fill 148 SMs several times over (2048 resident threads/SM)
 constexpr int64_t kTargetUnits = 148LL * 2048 * 3;
 constexpr int64_t kMinChunkDraws = 512;
@@ -444,12 +445,26 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
         nchunks = ceil_div(rows, rpc);
         const int64_t nunits = base * nchunks;
         const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
-        if (two)
-            fill_normal_fast<T, 2><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo, nrows_grid,
-                                                                 rpc, nunits, tab);
-        else
-            fill_normal_fast<T, 1><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo, nrows_grid,
-                                                                 rpc, nunits, tab);
+        // variant knob (tuning only): bit 0 -> cap registers (4 CTAs/SM),
+        // bit 1 -> one pair per thread even when two fit
+        const int v = tune_knob("SFB_NORMAL_VARIANT", kNormalVariantDefault);
+        if (two && !(v & 2)) {
+            if (v & 1)
+                fill_normal_fast<T, 2, 4><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                       nrows_grid, rpc, nunits, tab);
+            else
+                fill_normal_fast<T, 2, 1><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                       nrows_grid, rpc, nunits, tab);
+        } else {
+            const int64_t nunits1 = two ? nunits * 2 : nunits;
+            const unsigned blocks1 = (unsigned)ceil_div(nunits1, kThreads);
+            if (v & 1)
+                fill_normal_fast<T, 1, 4><<<blocks1, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                        nrows_grid, rpc, nunits1, tab);
+            else
+                fill_normal_fast<T, 1, 1><<<blocks1, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                        nrows_grid, rpc, nunits1, tab);
+        }
         return launch_check("fill_normal_fast");
     }
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);

@@ -150,8 +150,8 @@ struct LfShared {
 };
 
 // dynamic shared memory: exp table (2 KiB) | margins | [lf] | jwork
-template <bool LF_SMEM>
-__global__ void __launch_bounds__(kFisherThreads) fisher_kernel(const FisherArgs a,
+template <bool LF_SMEM, int MINB>
+__global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const FisherArgs a,
                                                          const __grid_constant__ ChunkJumps jumps) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *exptab = (uint64_t *)smem;
@@ -286,6 +286,16 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+template <bool LF_SMEM, int MINB>
+static cudaError_t launch_fisher(unsigned blocks, size_t smem, cudaStream_t st,
+                                 const FisherArgs &a, const ChunkJumps &jumps) {
+    cudaError_t e = cudaFuncSetAttribute(fisher_kernel<LF_SMEM, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fisher_kernel<LF_SMEM, MINB><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    return cudaGetLastError();
+}
+
 }  // namespace sfb
 
 using namespace sfb;
@@ -361,16 +371,23 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     const size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
     const unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
     if (smem > 200 * 1024) return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
+    // register cap: 4 CTAs/SM (64 regs) for walk-heavy wide tables, 3 (80
+    // regs) for small ones -- measured on B200 (tools/tune.py)
+    const int minb = tune_knob("SFB_FISHER_MINB", nr * nc >= 36 ? 4 : 3);
     if (lf_smem) {
-        e = cudaFuncSetAttribute(fisher_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        if (e == cudaSuccess)
-            fisher_kernel<true><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+        if (minb >= 4)
+            e = launch_fisher<true, 4>(blocks, smem, st, a, jumps);
+        else if (minb == 3)
+            e = launch_fisher<true, 3>(blocks, smem, st, a, jumps);
+        else
+            e = launch_fisher<true, 1>(blocks, smem, st, a, jumps);
     } else {
-        e = cudaFuncSetAttribute(fisher_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        if (e == cudaSuccess)
-            fisher_kernel<false><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+        if (minb >= 4)
+            e = launch_fisher<false, 4>(blocks, smem, st, a, jumps);
+        else if (minb == 3)
+            e = launch_fisher<false, 3>(blocks, smem, st, a, jumps);
+        else
+            e = launch_fisher<false, 1>(blocks, smem, st, a, jumps);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher kernel launch: %s", cudaGetErrorString(e));

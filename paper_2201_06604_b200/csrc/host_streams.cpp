@@ -101,6 +101,11 @@ void pow2_table(Pow2Table *t) {
 
 static const uint64_t kExpTable[256] = SFB_EXP_TABLE_INIT;
 
+int tune_knob(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
 }  // namespace sfb
 
 using namespace sfb;

@@ -16,4 +16,8 @@ void jump_pow(uint64_t n, Jump *out);       // A^n, exact
 void jump_pow2(int e, Jump *out);           // A^(2^e), exact, any e >= 0
 void pow2_table(Pow2Table *t);              // A^(2^b), b < kPow2Bits (cached)
 
+// integer tuning knob from the environment (kernel variant selection for
+// profiling sweeps; never changes results)
+int tune_knob(const char *name, int dflt);
+
 }  // namespace sfb

@@ -1,0 +1,83 @@
+"""Kernel-variant sweep (tuning knobs SFB_NORMAL_VARIANT / SFB_FISHER_MINB).
+
+    python tools/tune.py [normal] [fisher]
+
+Prints one line per (workload, variant) with the CUDA-event time per launch.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2201_06604_b200 as sf  # noqa: E402
+from paper_2201_06604_b200.fisher import launch_fisher, plan_fisher  # noqa: E402
+from paper_2201_06604_b200.grid import launch_fill  # noqa: E402
+
+T4 = [[5, 9, 5, 7], [9, 5, 9, 7], [8, 6, 2, 6], [10, 8, 8, 8]]
+
+
+def timeit(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def normal_case(dtype):
+    st = sf.create_streams(sf.set_base_creator(), 1 << 18)[0]
+    cur = st.device_current()
+    out = torch.empty((31250, 32000), dtype=dtype, device="cuda")
+    return lambda: launch_fill("normal", cur, st.count, out, 31250, 32000, 32000, 512, 512)
+
+
+def fisher_case(table, n, g):
+    grid = sf.WorkGrid(*g)
+    st = sf.create_streams(sf.set_base_creator(), grid.size)[0]
+    plan = plan_fisher(np.asarray(table), n, st, grid)
+    cur = st.device_current()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    return plan.sim_num, lambda: launch_fisher(plan, cur, st.count, cnt)
+
+
+def main():
+    what = sys.argv[1:] or ["normal", "fisher"]
+    res = []
+    if "normal" in what:
+        for dt in (torch.float32, torch.float64):
+            fn = normal_case(dt)
+            for v in (0, 1, 2, 3):
+                os.environ["SFB_NORMAL_VARIANT"] = str(v)
+                ms = timeit(fn)
+                res.append({"w": f"normal_{str(dt)[6:]}", "variant": v, "ms": ms,
+                            "per_s": 1e9 / (ms / 1e3)})
+                print(json.dumps(res[-1]), flush=True)
+        os.environ.pop("SFB_NORMAL_VARIANT")
+    if "fisher" in what:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
+            t10 = np.array(json.load(fh)["T10"])
+        for name, table, n, g in (("T4", T4, 10 ** 6, (256, 64)),
+                                  ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
+                                  ("T10", t10, 1 << 23, (2048, 1024))):
+            sim, fn = fisher_case(table, n, g)
+            for mb in (1, 3, 4):
+                os.environ["SFB_FISHER_MINB"] = str(mb)
+                ms = timeit(fn, reps=3, warm=1)
+                res.append({"w": f"fisher_{name}", "variant": mb, "ms": ms,
+                            "per_s": sim / (ms / 1e3)})
+                print(json.dumps(res[-1]), flush=True)
+
+
+if __name__ == "__main__":
+    main()
