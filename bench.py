@@ -115,11 +115,10 @@ class ClockSampler:
 
 
 def shard(n, rank, world, align=1):
-    """contiguous block [lo, hi) of n units for `rank`, boundaries multiple of align"""
-    units = n // align
-    lo = units * rank // world * align
-    hi = units * (rank + 1) // world * align
-    return lo, hi
+    """contiguous block [lo, hi) of n units for `rank` (paper_2201_06604_b200.sharding)"""
+    from paper_2201_06604_b200.sharding import shard_range
+
+    return shard_range(n, rank, world, align)
 
 
 class Timer:

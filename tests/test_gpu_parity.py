@@ -441,3 +441,21 @@ def test_checkpoint_continuation_c5_full(tmp_path):
     b = sf.run_grid(st2, g, 32768, 65536, "uniform")
     assert torch.equal(b.tensor, full.tensor[32768:])
     assert st2 == st_full
+
+
+def test_sharded_api_single_rank(A):
+    # the multi-GPU entry points on one device (world size 1, no collective)
+    from paper_2201_06604_b200 import sharding
+
+    st = fresh(64)
+    r = sharding.fisher_sim_sharded(A["month"], 3000, st, sf.WorkGrid(8, 8), return_stats=True)
+    ref_st = oa.fresh_states(64)
+    ref = oa.fisher(A["month"], 3000, ref_st, (8, 8), return_stats=True)
+    assert r.counts == ref["counts"]
+    assert np.array_equal(r.statistics, ref["statistics"])
+    assert np.array_equal(st.current, ref_st)
+    st = fresh(64)
+    buf = sharding.run_grid_sharded(st, sf.WorkGrid(8, 8), 100, 120, "uniform")
+    ref_st = oa.fresh_states(64)
+    assert np.array_equal(buf.data, oa.fill("uniform", ref_st, (100, 120), (8, 8)))
+    assert np.array_equal(st.current, ref_st)
