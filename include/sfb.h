@@ -142,6 +142,13 @@ double sfb_host_exp(double x);
  * for draws z1[k], z2[k] in [1, m1]: a = R cos(theta), b = R cos(theta - pi/2) */
 int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,
                         double *b);
+/* the device Fisher sampler (fisher_sampler.cuh) run serially on the host over
+ * items [item_lo, item_hi) (states int64 (n,6), mutated; stats nullable,
+ * indexed (w - item_lo)*reps + rep; *count = hits) -- CPU test hook */
+int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr,
+                               const int64_t *ncolt, int nc, const double *lf,
+                               double threshold, int64_t reps, int64_t item_lo,
+                               int64_t item_hi, double *stats, int64_t *count);
 
 #ifdef __cplusplus
 }

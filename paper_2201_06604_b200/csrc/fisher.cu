@@ -31,11 +31,13 @@
 #include <vector>
 
 #include "exp_glibc.cuh"
+#include "fisher_sampler.cuh"
 #include "sfb_internal.h"
 
 namespace sfb {
 
 constexpr int kMaxChunks = 96;
+constexpr int kFisherWalkDefault = 1;  // fisher_sampler.cuh walk form (tools/tune.py)
 constexpr int kFisherThreads = 256;
 
 struct ChunkJumps {
@@ -55,102 +57,14 @@ struct FisherArgs {
     int nr, nc, ntot, lf_len;
 };
 
-// one conditional hypergeometric draw (_kernels.py:205-261); consumes one step
-template <typename LF>
-__device__ __forceinline__ int sample_cell(int ia, int idv, int ie, int ib, int ic, int ii,
-                                           const LF &lf, const uint64_t *exptab, Mrg &s) {
-    const uint32_t zm1 = step_m1(s);  // _kernels.py:211-212: u = z * NORM, exact
-    const double u = __fma_rn((double)zm1, kNorm, kNorm);
-    int lo = ia + idv - ie;
-    if (lo < 0) lo = 0;
-    const int hi = ia < idv ? ia : idv;
-    if (hi <= lo) return lo;  // forced cell: the uniform is still consumed
-    // start the CDF inversion near the mode (_kernels.py:221-225)
-    int k = (int)((double)ia * ((double)idv / (double)ie) + 0.5);
-    if (k < lo)
-        k = lo;
-    else if (k > hi)
-        k = hi;
-    const double base = lf(ia) + lf(ib) + lf(idv) + lf(ic) - lf(ie);  // :226
-    const double x = glibc_exp(base - lf(k) - lf(idv - k) - lf(ia - k) - lf(ii + k), exptab);
-    if (!(u > x)) return k;
-    // walk outward, alternating up and down (_kernels.py:230-261)
-    double acc = x, pu = x, pd = x;
-    int ku = k, kd = k;
-    for (;;) {
-        bool moved = false;
-        if (ku < hi) {
-            pu = pu * (double)(idv - ku) * (double)(ia - ku) /
-                 (((double)ku + 1.0) * ((double)(ii + ku) + 1.0));
-            ku += 1;
-            acc += pu;
-            moved = true;
-            if (u <= acc) return ku;
-        }
-        if (kd > lo) {
-            pd = pd * (double)kd * (double)(ii + kd) /
-                 (((double)(idv - kd) + 1.0) * ((double)(ia - kd) + 1.0));
-            kd -= 1;
-            acc += pd;
-            moved = true;
-            if (u <= acc) return kd;
-        }
-        if (!moved) return ku;  // round-off leftover: take an endpoint
-    }
-}
-
-// sample one table and return its statistic; jw = per-thread column work
-// array (stride `js`), mat (nullable) receives the table (rcont2)
-template <typename LF>
-__device__ __forceinline__ double sample_table(const int32_t *rowm, const int32_t *colm, int nr,
-                                               int nc, int ntot, const LF &lf,
-                                               const uint64_t *exptab, Mrg &s, int *jw, int js,
-                                               int64_t *mat) {
-    double stat = 0.0;
-    int jc = ntot;
-    for (int m = 0; m < nc - 1; ++m) jw[m * js] = colm[m];
-    for (int l = 0; l < nr - 1; ++l) {
-        int ia = rowm[l];
-        int ic = jc;
-        jc -= ia;
-        for (int m = 0; m < nc - 1; ++m) {
-            const int idv = jw[m * js];
-            const int ie = ic;
-            ic -= idv;
-            const int ib = ie - ia;
-            const int ii = ib - idv;
-            const int k = sample_cell(ia, idv, ie, ib, ic, ii, lf, exptab, s);
-            stat -= lf(k);  // row-major order of _kernels.py:271-274
-            if (mat) mat[l * nc + m] = k;
-            ia -= k;
-            jw[m * js] = idv - k;
-        }
-        stat -= lf(ia);  // mat[l, nc-1] = ia
-        if (mat) mat[l * nc + nc - 1] = ia;
-    }
-    int rem = rowm[nr - 1];
-    for (int m = 0; m < nc - 1; ++m) {
-        const int v = jw[m * js];
-        stat -= lf(v);
-        if (mat) mat[(nr - 1) * nc + m] = v;
-        rem -= v;
-    }
-    stat -= lf(rem);
-    if (mat) mat[(nr - 1) * nc + nc - 1] = rem;
-    return stat;
-}
-
 struct LfGlobal {
     const double *p;
     __device__ __forceinline__ double operator()(int k) const { return __ldg(p + k); }
 };
-struct LfShared {
-    const double *p;
-    __device__ __forceinline__ double operator()(int k) const { return p[k]; }
-};
+using LfShared = LfPlain;
 
 // dynamic shared memory: exp table (2 KiB) | margins | [lf] | jwork
-template <bool LF_SMEM, int MINB>
+template <bool LF_SMEM, int MINB, int WALK>
 __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const FisherArgs a,
                                                          const __grid_constant__ ChunkJumps jumps) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -183,10 +97,10 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
             for (int64_t rep = rep0; rep < rep1; ++rep) {
                 double stat;
                 if (LF_SMEM)
-                    stat = sample_table(rowm, colm, a.nr, a.nc, a.ntot, LfShared{lfs}, exptab, s,
+                    stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, LfShared{lfs}, exptab, s,
                                         jw, blockDim.x, nullptr);
                 else
-                    stat = sample_table(rowm, colm, a.nr, a.nc, a.ntot, LfGlobal{a.lf}, exptab,
+                    stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, LfGlobal{a.lf}, exptab,
                                         s, jw, blockDim.x, nullptr);
                 if (stat <= a.threshold) ++hits;  // _kernels.py:275-276
                 if (a.stats) a.stats[local * a.reps + rep] = stat;
@@ -220,7 +134,8 @@ __global__ void rcont2_kernel(const int32_t *rowm, const int32_t *colm, int nr, 
     } else if (nc == 1) {
         for (int l = 0; l < nr; ++l) mat[l] = rowm[l];
     } else {
-        sample_table(rowm, colm, nr, nc, ntot, LfGlobal{lf}, exptab, s, jw, 1, mat);
+        sample_table<kFisherWalkDefault>(rowm, colm, nr, nc, ntot, LfGlobal{lf}, exptab, s, jw, 1,
+                                          mat);
     }
     store_state(state, s);
 }
@@ -286,14 +201,24 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+template <bool LF_SMEM, int MINB, int WALK>
+static cudaError_t launch_fisher_walk(unsigned blocks, size_t smem, cudaStream_t st,
+                                      const FisherArgs &a, const ChunkJumps &jumps) {
+    cudaError_t e = cudaFuncSetAttribute(fisher_kernel<LF_SMEM, MINB, WALK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fisher_kernel<LF_SMEM, MINB, WALK><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    return cudaGetLastError();
+}
+
 template <bool LF_SMEM, int MINB>
 static cudaError_t launch_fisher(unsigned blocks, size_t smem, cudaStream_t st,
                                  const FisherArgs &a, const ChunkJumps &jumps) {
-    cudaError_t e = cudaFuncSetAttribute(fisher_kernel<LF_SMEM, MINB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    fisher_kernel<LF_SMEM, MINB><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
-    return cudaGetLastError();
+    switch (tune_knob("SFB_FISHER_WALK", kFisherWalkDefault)) {
+        case 0: return launch_fisher_walk<LF_SMEM, MINB, 0>(blocks, smem, st, a, jumps);
+        case 2: return launch_fisher_walk<LF_SMEM, MINB, 2>(blocks, smem, st, a, jumps);
+        default: return launch_fisher_walk<LF_SMEM, MINB, 1>(blocks, smem, st, a, jumps);
+    }
 }
 
 }  // namespace sfb
@@ -373,7 +298,7 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     if (smem > 200 * 1024) return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
     // register cap: 4 CTAs/SM (64 regs) for walk-heavy wide tables, 3 (80
     // regs) for small ones -- measured on B200 (tools/tune.py)
-    const int minb = tune_knob("SFB_FISHER_MINB", nr * nc >= 36 ? 4 : 3);
+    const int minb = tune_knob("SFB_FISHER_MINB", 4);
     if (lf_smem) {
         if (minb >= 4)
             e = launch_fisher<true, 4>(blocks, smem, st, a, jumps);

@@ -18,8 +18,10 @@
 
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "box_muller.cuh"
+#include "fisher_sampler.cuh"
 #include "exp_glibc.cuh"
 #include "sfb_internal.h"
 
@@ -448,6 +450,35 @@ int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out)
 }
 
 double sfb_host_exp(double x) { return glibc_exp(x, kExpTable); }
+
+int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const int64_t *ncolt,
+                               int nc, const double *lf, double threshold, int64_t reps,
+                               int64_t item_lo, int64_t item_hi, double *stats,
+                               int64_t *count) {
+    std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
+    std::vector<int> jw(nc > 1 ? nc - 1 : 1);
+    int64_t ntot = 0;
+    for (int l = 0; l < nr; ++l) ntot += nrowt[l];
+    int64_t hits = 0;
+    for (int64_t w = item_lo; w < item_hi; ++w) {
+        Mrg s = load_state(cur + 6 * w);
+        for (int64_t rep = 0; rep < reps; ++rep) {
+            const int walk = tune_knob("SFB_FISHER_WALK", 1);
+            const double stat =
+                walk == 0 ? sample_table<0>(rowm.data(), colm.data(), nr, nc, (int)ntot,
+                                            LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
+                : walk == 2 ? sample_table<2>(rowm.data(), colm.data(), nr, nc, (int)ntot,
+                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
+                            : sample_table<1>(rowm.data(), colm.data(), nr, nc, (int)ntot,
+                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr);
+            hits += stat <= threshold;
+            if (stats) stats[(w - item_lo) * reps + rep] = stat;
+        }
+        store_state(cur + 6 * w, s);
+    }
+    *count = hits;
+    return SFB_OK;
+}
 
 int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,
                         double *b) {

@@ -374,3 +374,44 @@ def test_box_muller_port_against_libm():
         d = np.abs(g32.astype(np.float64) - r32.astype(np.float64))
         assert (d <= np.spacing(np.abs(r32)).astype(np.float64)).all()
         assert eq.mean() >= 0.99999, eq.mean()
+
+
+def _host_fisher(table, n, n_items, reps_override=None, stats=False):
+    from scipy.special import gammaln
+
+    t = np.asarray(table, np.int64)
+    lf = gammaln(np.arange(t.sum() + 1, dtype=np.float64) + 1.0)
+    thr = float(-gammaln(t + 1.0).sum())
+    thr = thr + 1e-7 * abs(thr)
+    reps = reps_override or -(-n // n_items)
+    rows, _ = orc.create_streams(sf.DEFAULT_SEED, n_items)
+    cur = rows.copy()
+    out = np.empty(n_items * reps) if stats else None
+    cnt = np.zeros(1, np.int64)
+    rm, cm = np.ascontiguousarray(t.sum(1)), np.ascontiguousarray(t.sum(0))
+    _lib.check(_lib.lib().sfb_host_fisher_replicates(
+        _lib.ptr(cur), _lib.ptr(rm), len(rm), _lib.ptr(cm), len(cm), _lib.ptr(lf, _lib._f64p),
+        thr, reps, 0, n_items, None if out is None else _lib.ptr(out, _lib._f64p),
+        _lib.ptr(cnt)))
+    ref = rows.copy()
+    rstats = np.empty(n_items * reps) if stats else None
+    rcnt = orc.fisher_replicates(ref, rm, cm, lf, thr, reps, n_items, rstats)
+    return int(cnt[0]), rcnt, cur, ref, out, rstats
+
+
+@pytest.mark.parametrize("name", ["T10", "month", "T4", "week"])
+def test_device_fisher_sampler_on_host_matches_oracle(G, A, name):
+    """The device sampler source (fisher_sampler.cuh: Markstein walk, exact
+    double counters, glibc exp port) run on the host == oracle, bit for bit."""
+    table = {"T10": G["T10"], "T4": G["T4"], "month": A["month"], "week": A["week"]}[name]
+    cnt, rcnt, cur, ref, st, rst = _host_fisher(table, 0, 64, reps_override=40, stats=True)
+    assert cnt == rcnt
+    assert np.array_equal(cur, ref)
+    assert np.array_equal(st, rst)
+
+
+@pytest.mark.parametrize("key", ["F_E2x2", "F_E2x5", "F_E5x2", "F_Ezero_col", "F_Eones", "F_Ebig"])
+def test_device_fisher_sampler_edge_tables(A, key):
+    t = A["tab_" + key[2:]]
+    cnt, rcnt, cur, ref, st, rst = _host_fisher(t, 0, 16, reps_override=200, stats=True)
+    assert cnt == rcnt and np.array_equal(cur, ref) and np.array_equal(st, rst)

@@ -71,12 +71,14 @@ def main():
                                   ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
                                   ("T10", t10, 1 << 23, (2048, 1024))):
             sim, fn = fisher_case(table, n, g)
-            for mb in (1, 3, 4):
-                os.environ["SFB_FISHER_MINB"] = str(mb)
-                ms = timeit(fn, reps=3, warm=1)
-                res.append({"w": f"fisher_{name}", "variant": mb, "ms": ms,
-                            "per_s": sim / (ms / 1e3)})
-                print(json.dumps(res[-1]), flush=True)
+            for walk in (0, 1, 2):
+                for mb in (3, 4):
+                    os.environ["SFB_FISHER_MINB"] = str(mb)
+                    os.environ["SFB_FISHER_WALK"] = str(walk)
+                    ms = timeit(fn, reps=3, warm=1)
+                    res.append({"w": f"fisher_{name}", "variant": f"walk{walk}_minb{mb}",
+                                "ms": ms, "per_s": sim / (ms / 1e3)})
+                    print(json.dumps(res[-1]), flush=True)
 
 
 if __name__ == "__main__":
