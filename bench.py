@@ -385,6 +385,46 @@ def _t10():
         return json.load(fh)["T10"]
 
 
+def run_probes(torch, _lib):
+    """Roofline denominators MEASURED_PEAKS.json lacks: write-only HBM
+    bandwidth (torch fill of 16 GiB) and the FP64 pipe (sfb_probe_fp64:
+    8 independent DFMA chains per thread, 8 CTAs of 256 per SM)."""
+    out = {}
+    buf = torch.empty(16 << 30, dtype=torch.uint8, device="cuda")
+    tm = Timer(torch)
+    best = None
+    for _ in range(4):
+        tm.start()
+        buf.fill_(1)
+        ms = tm.stop()
+        best = ms if best is None else min(best, ms)
+    out["hbm_write_gbs"] = buf.numel() / (best / 1e3) / 1e9
+    del buf
+    d = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks, iters = 148 * 8, 4096
+    st = _lib.stream_handle()
+    _lib.check(_lib.lib().sfb_probe_fp64(_lib.dptr(d), blocks, iters, st))
+    best = None
+    for _ in range(3):
+        tm.start()
+        _lib.check(_lib.lib().sfb_probe_fp64(_lib.dptr(d), blocks, iters, st))
+        ms = tm.stop()
+        best = ms if best is None else min(best, ms)
+    out["fp64_ops_per_s"] = blocks * 256 * iters * 8 / (best / 1e3)  # DFMA/s (1 op each)
+    return out
+
+
+def ncu_traffic(kernel):
+    """dram read+write bytes per algorithmic byte from the committed ncu capture
+    (profiles/traffic.json, written by tools/summarize_ncu.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)[kernel]
+        return t["dram_bytes"] / t["alg_bytes"], t["source"]
+    except Exception:
+        return None, None
+
+
 # ---------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -409,6 +449,7 @@ def main():
     _lib.require_device()
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2, for flushes
     peak, peak_kind = peaks()
+    probe = run_probes(torch, _lib)
 
     prim = run_uniform(torch, sf, rank, world, args.steps, args.warmup, C5)
     workloads = {}
@@ -444,7 +485,25 @@ def main():
 
     if rank != 0:
         return
+    # per-workload rooflines against the probes measured above
+    wpeak = probe["hbm_write_gbs"]
+    if "rnormGpu_f32_1e9" in workloads:
+        w = workloads["rnormGpu_f32_1e9"]
+        w["roofline"] = {"bound": "hbm", "achieved": w["gbs"], "unit": "GB/s",
+                         "peak_copy": peak, "frac_copy": w["gbs"] / peak,
+                         "peak_write": wpeak, "frac_write": w["gbs"] / wpeak,
+                         "note": "compute/issue bound: ~131 SASS (45 FP64) per normal pair"}
+    for key, fops in (("fisher_T4_1e6", FOPS["T4"]), ("fisher_T10", FOPS["T10"])):
+        if key in workloads:
+            w = workloads[key]
+            ach = w["value"] * fops
+            w["roofline"] = {"bound": "fp64", "achieved": ach / 1e12, "unit": "Tops/s",
+                             "peak": probe["fp64_ops_per_s"] / 1e12,
+                             "frac": ach / probe["fp64_ops_per_s"],
+                             "note": "source-level FP64 ops per table (SURVEY 8(d)) vs the "
+                                     "measured DFMA issue rate (sfb_probe_fp64)"}
     achieved = prim["alg_bytes"] / (prim["launch_ms"] / 1e3) / 1e9
+    tr_ratio, tr_src = ncu_traffic("fill_uniform_fast")
     line = {
         "metric": METRIC, "value": prim["value"], "unit": "uniforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": prim["ms_per_step"],
@@ -456,10 +515,14 @@ def main():
                    "l2": "output 34.4 GB per step >> 126 MB L2 (no flush needed)",
                    "parallelism": f"stream-ordinal blocks x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak,
+                     "traffic": None if tr_ratio is None else tr_ratio * prim["alg_bytes"],
+                     "traffic_source": tr_src,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "peak_write_measured": wpeak, "frac_write": achieved / wpeak,
                      "kernel": "fill_uniform_fast<0>",
                      "algorithmic_bytes_per_launch": prim["alg_bytes"]},
+        "probes": probe,
         "clocks": prim["clocks"],
         "gpu_launches": prim["launches"],
         "workloads": workloads,

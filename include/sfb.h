@@ -132,6 +132,10 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
                      const double *lf, int64_t lf_len, int64_t *d_state,
                      int64_t *d_mat, void *stream);
 
+/* ---- measurement ---------------------------------------------------------- */
+/* FP64-pipe roofline probe (bench.py): blocks x 256 threads x iters x 8 DFMA */
+int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream);
+
 /* ---- test hooks (host execution of the device arithmetic) --------------- */
 /* runs the uint32 device step formulation on the host: n states x steps,
  * writes the outputs z and advances states (int64 (n,6)) */

@@ -296,8 +296,8 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     const size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
     const unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
     if (smem > 200 * 1024) return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
-    // register cap: 4 CTAs/SM (64 regs) for walk-heavy wide tables, 3 (80
-    // regs) for small ones -- measured on B200 (tools/tune.py)
+    // register cap: 4 CTAs/SM (64 regs) -- best for every table measured on
+    // B200 (tools/tune.py sweep of 3 walk forms x {3, 4} CTAs/SM)
     const int minb = tune_knob("SFB_FISHER_MINB", 4);
     if (lf_smem) {
         if (minb >= 4)

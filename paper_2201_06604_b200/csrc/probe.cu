@@ -1,0 +1,38 @@
+// probe.cu -- roofline probes used by bench.py (not part of the hot path).
+//
+// MEASURED_PEAKS.json has the copy bandwidth and the bf16 tensor peak; the
+// Fisher kernel is bound by the FP64 pipe, whose peak this probe measures:
+// every thread runs 8 independent DFMA chains (enough ILP to cover the FP64
+// latency), so the kernel issues DFMA at the pipe's throughput limit.
+#include <cuda_runtime.h>
+
+#include "sfb_internal.h"
+
+namespace sfb {
+
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double *out, int iters, double a,
+                                                         double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __fma_rn(x[k], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream) {
+    fp64_probe_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_out, iters,
+                                                                          0.999999, 1e-7);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "fp64 probe: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}

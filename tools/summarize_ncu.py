@@ -107,6 +107,27 @@ def main():
                  "B200 via tools/gpu_profile.sh (driver: tools/prof_driver.py).\n\n")
         for rep in args:
             fh.write(summarize(rep) + "\n")
+    # traffic per algorithmic byte for the HBM-bound kernels (bench.py reads it)
+    alg = {"uniform": ("fill_uniform_fast", 4096 * 65536 * 8 + (1 << 20) * 96),
+           "normal": ("fill_normal_fast", (31250 // 8) * 32000 * 4 + (1 << 18) * 96)}
+    traffic = {}
+    for rep in args:
+        for key, (kname, abytes) in alg.items():
+            if f"prof_{key}_" in os.path.basename(rep):
+                raw = ncu_csv(rep, "raw")
+                m = dict(zip(raw[0], raw[2]))
+                u = dict(zip(raw[0], raw[1]))
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                tot = sum(float(m[k].replace(",", "")) * scale.get(u[k], 1)
+                          for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                traffic[kname] = {"dram_bytes": tot, "alg_bytes": abytes,
+                                  "source": f"profiles/{tag}/ncu_summary.md "
+                                            f"({os.path.basename(rep)}, tools/prof_driver.py {key})"}
+    if traffic:
+        with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
+            import json
+
+            json.dump(traffic, fh, indent=1)
     if lcsv:
         import shutil
 
