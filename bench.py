@@ -387,22 +387,22 @@ def _t10():
 
 def run_probes(torch, _lib):
     """Roofline denominators MEASURED_PEAKS.json lacks: write-only HBM
-    bandwidth (torch fill of 16 GiB) and the FP64 pipe (sfb_probe_fp64:
+    bandwidth (sfb_probe_write: 16-byte streaming stores over 16 GiB) and the FP64 pipe (sfb_probe_fp64:
     8 independent DFMA chains per thread, 8 CTAs of 256 per SM)."""
     out = {}
     buf = torch.empty(16 << 30, dtype=torch.uint8, device="cuda")
     tm = Timer(torch)
     best = None
+    st = _lib.stream_handle()
     for _ in range(4):
         tm.start()
-        buf.fill_(1)
+        _lib.check(_lib.lib().sfb_probe_write(_lib.dptr(buf), buf.numel(), st))
         ms = tm.stop()
         best = ms if best is None else min(best, ms)
     out["hbm_write_gbs"] = buf.numel() / (best / 1e3) / 1e9
     del buf
     d = torch.zeros(1, dtype=torch.float64, device="cuda")
     blocks, iters = 148 * 8, 4096
-    st = _lib.stream_handle()
     _lib.check(_lib.lib().sfb_probe_fp64(_lib.dptr(d), blocks, iters, st))
     best = None
     for _ in range(3):

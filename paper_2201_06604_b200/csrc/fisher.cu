@@ -190,9 +190,8 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
     e = cudaMemcpyAsync(scr.p, host.data(), bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "margins upload: %s", cudaGetErrorString(e));
-    // pageable source: make sure the staging copy finished before `host` dies
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return fail(SFB_E_CUDA, "margins upload: %s", cudaGetErrorString(e));
+    // pageable source: cudaMemcpyAsync returns once `host` has been copied to the
+    // driver's staging memory, so `host` may be freed on return (no sync needed)
     *rowm = (int32_t *)scr.p;
     *colm = *rowm + nr;
     *lfd = (double *)((unsigned char *)scr.p + lf_off);
@@ -268,7 +267,11 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     const int64_t rpc = ceil_div(reps, nchunks);
     nchunks = ceil_div(reps, rpc);
     ChunkJumps jumps;
-    for (int64_t c = 0; c < nchunks; ++c) jump_pow((uint64_t)(c * rpc * F), &jumps.j[c]);
+    // J_c = A^(c rpc F): one exact power, then one product per chunk
+    Jump step;
+    jump_pow((uint64_t)(rpc * F), &step);
+    jump_pow(0, &jumps.j[0]);
+    for (int64_t c = 1; c < nchunks; ++c) jump_mul(jumps.j[c - 1], step, &jumps.j[c]);
 
     FisherArgs a;
     a.cur = d_cur;

@@ -72,6 +72,8 @@ static void jump_mul(const Jump &a, const Jump &b, Jump &o) {
     mat_mul(a.p2, b.p2, kM2, o.p2);
 }
 
+void jump_mul(const Jump &a, const Jump &b, Jump *o) { jump_mul(a, b, *o); }
+
 void jump_pow2(int e, Jump *out) {  // core.py:55-62
     Jump j = base_jump();
     for (int k = 0; k < e; ++k) jump_mul(j, j, j);

@@ -25,9 +25,24 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double *out, int iters,
     if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// write-only HBM probe: 16-byte streaming stores, grid-stride
+__global__ void __launch_bounds__(256) write_probe_kernel(double2 *out, int64_t n) {
+    const double2 v = make_double2(1.0, 2.0);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        __stcs(out + i, v);
+}
+
 }  // namespace sfb
 
 using namespace sfb;
+
+extern "C" int sfb_probe_write(void *d_out, int64_t bytes, void *stream) {
+    write_probe_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>((double2 *)d_out, bytes / 16);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "write probe: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
 
 extern "C" int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream) {
     fp64_probe_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_out, iters,

@@ -14,6 +14,7 @@ int fail(int code, const char *fmt, ...);
 // transition matrices _T1/_T2 (core.py:44-45) raised to arbitrary powers
 void jump_pow(uint64_t n, Jump *out);       // A^n, exact
 void jump_pow2(int e, Jump *out);           // A^(2^e), exact, any e >= 0
+void jump_mul(const Jump &a, const Jump &b, Jump *out);  // a*b (powers of A commute)
 void pow2_table(Pow2Table *t);              // A^(2^b), b < kPow2Bits (cached)
 
 // integer tuning knob from the environment (kernel variant selection for
