@@ -31,6 +31,7 @@
 #include <algorithm>
 
 #include "box_muller.cuh"
+#include "log1p_glibc.cuh"
 #include "sfb_internal.h"
 
 namespace sfb {
@@ -55,7 +56,7 @@ template <int KIND>
 __device__ __forceinline__ double real_value(uint32_t zm1, double rate) {
     const double u = u01(zm1);
     if (KIND == kUniform) return u;
-    return __ddiv_rn(-log1p(-u), rate);  // _kernels.py:74 (CUDA log1p: tolerance, not bit-exact)
+    return __ddiv_rn(-glibc_log1p(-u), rate);  // _kernels.py:74, glibc log1p port: bit-exact
 }
 
 // one 16-byte streaming store of a column pair / one 8-byte store

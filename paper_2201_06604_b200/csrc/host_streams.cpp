@@ -22,6 +22,7 @@
 
 #include "box_muller.cuh"
 #include "fisher_sampler.cuh"
+#include "log1p_glibc.cuh"
 #include "exp_glibc.cuh"
 #include "sfb_internal.h"
 
@@ -452,6 +453,8 @@ int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out)
 }
 
 double sfb_host_exp(double x) { return glibc_exp(x, kExpTable); }
+
+double sfb_host_log1p(double x) { return glibc_log1p(x); }
 
 int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const int64_t *ncolt,
                                int nc, const double *lf, double threshold, int64_t reps,
