@@ -8,7 +8,7 @@ Bars:
     four draws z2 = k 2^29 where theta is pi/2-multiple-adjacent);
   * Box-Muller float32: |gpu - float32(ref)| <= 1 ulp_f32 everywhere, and
     identical on >= 99.999 % of cells;
-  * exponential: |gpu - ref| <= 4 ulp(ref) (CUDA log1p vs glibc log1p).
+  * exponential: bit-exact (glibc log1p FMA-variant port, log1p_glibc.cuh).
 """
 
 import math
@@ -247,7 +247,7 @@ def test_exponential_small(G, rate):
     buf = sf.fill_exponential(st, sf.FillRequest(shape=(2, 4), kind="exponential", rate=rate,
                                                  grid=sf.WorkGrid(2, 2)))
     ref = np.array(G[f"E24_{rate}"]["values"])
-    assert (np.abs(buf.values - ref) <= 4 * ulp64(ref)).all()
+    assert np.array_equal(buf.values, ref)
     assert st.current.tolist() == G[f"E24_{rate}"]["states"]
 
 
@@ -256,7 +256,7 @@ def test_exponential_big(A):
     buf = sf.fill_exponential(st, sf.FillRequest(shape=(100, 100), kind="exponential",
                                                  rate=1.5, grid=sf.WorkGrid(4, 4)))
     ref = A["E100_data"]
-    assert (np.abs(buf.data - ref) <= 4 * ulp64(ref)).all()
+    assert np.array_equal(buf.data, ref)
     assert np.array_equal(st.current, A["E100_states"])
 
 
@@ -458,4 +458,17 @@ def test_sharded_api_single_rank(A):
     buf = sharding.run_grid_sharded(st, sf.WorkGrid(8, 8), 100, 120, "uniform")
     ref_st = oa.fresh_states(64)
     assert np.array_equal(buf.data, oa.fill("uniform", ref_st, (100, 120), (8, 8)))
+    assert np.array_equal(st.current, ref_st)
+
+
+@pytest.mark.parametrize("shape,g,n,rate", [((257, 300), (16, 16), 256, 0.7),
+                                            ((64, 4096), (8, 512), 4096, 3.0),
+                                            (5001, (1, 64), 64, 1.0)])
+def test_exponential_layouts_bit_exact(shape, g, n, rate):
+    st = fresh(n)
+    buf = sf.fill_exponential(st, sf.FillRequest(shape=shape, kind="exponential", rate=rate,
+                                                 grid=sf.WorkGrid(*g)))
+    ref_st = oa.fresh_states(n)
+    ref = oa.fill("exponential", ref_st, shape, g, rate=rate)
+    assert np.array_equal(buf.data, ref)
     assert np.array_equal(st.current, ref_st)

@@ -133,6 +133,23 @@ def test_exp_port_bit_exact_against_libm():
     assert not bad, bad[:10]
 
 
+def test_log1p_port_bit_exact_against_libm():
+    libm = ctypes.CDLL(ctypes.util.find_library("m"))
+    libm.log1p.argtypes = [ctypes.c_double]
+    libm.log1p.restype = ctypes.c_double
+    port = _lib.lib().sfb_host_log1p
+    rng = np.random.default_rng(3)
+    xs = list(-(rng.integers(1, 2 ** 31, 100000) * 2.0 ** -31))  # the fill's arguments
+    xs += list(rng.uniform(-1, 1, 50000)) + list(np.exp(rng.uniform(-700, 700, 20000)))
+    xs += list(-np.exp(rng.uniform(-60, 0, 20000)))
+    xs += [0.0, -0.0, 1e-300, -1e-300, 2.0 ** -54, -(2.0 ** -54), 2.0 ** -29, -(2.0 ** -29),
+           0.41422, -0.2929, -0.29289321881345254, 1.0, -1.0, 2.0 ** 53, 2.0 ** 60, math.inf,
+           -math.inf, math.nan, -0.999999, 5e-324, -1.5]
+    bad = [x for x in xs if _bits(port(x)) != _bits(libm.log1p(x))
+           and not (math.isnan(port(x)) and math.isnan(libm.log1p(x)))]
+    assert not bad, bad[:10]
+
+
 def test_printed_matrix_and_goldens(G):
     s4 = sf.create_streams(sf.set_base_creator(), 4)[0]
     assert np.array_equal(s4.matrix(), PRINTED_STREAM_MATRIX)
