@@ -316,13 +316,25 @@ def cpu_uniform_sample(orc, rows, threads=0):
 
 
 def cpu_baseline(reps=3, rows=2048):
+    """The reference's CPU path on a bounded C5 sample: the unmodified numba
+    reference from baseline/_ref when installed, else the oracle C port."""
     from oracle import oracle as orc
 
     orc.lib()
+    n = rows * C5["ncol"]
+    sampler = numba_fill_sampler(rows)
+    if sampler is not None:
+        best = n / min(sampler() for _ in range(reps))
+        return {"value": best, "unit": "uniforms/s",
+                "cores": int(os.environ.get("NUMBA_NUM_THREADS", os.cpu_count())),
+                "kind": "reference",
+                "sample": f"C5 rows [0,{rows}) = {n} float64 uniforms from all 2^20 streams "
+                          f"(unmodified streamforge numba _kernels.fill_real, baseline/_ref), "
+                          f"best of {reps}"}
     cpu_uniform_sample(orc, 64)  # warm
     best = max(cpu_uniform_sample(orc, rows)[0] for _ in range(reps))
     return {"value": best, "unit": "uniforms/s", "cores": orc.max_threads(), "kind": "port",
-            "sample": f"C5 rows [0,{rows}) = {rows * C5['ncol']} float64 uniforms from all "
+            "sample": f"C5 rows [0,{rows}) = {n} float64 uniforms from all "
                       f"2^20 streams (oracle C port of _kernels.fill_real, OpenMP), best of {reps}"}
 
 
@@ -347,15 +359,17 @@ def reference_arm(args, rank, world):
 
     orc.lib()
     rows = 2048
-    cpu_uniform_sample(orc, 64)
+    n = rows * C5["ncol"]
+    numba_fill = numba_fill_sampler(rows)
+    kind = "reference" if numba_fill else "port"
+    sample = numba_fill or (lambda: cpu_uniform_sample(orc, rows)[1])
     for _ in range(args.warmup):
-        cpu_uniform_sample(orc, rows)
+        sample()
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_uniform_sample(orc, rows)[1])
+        vals.append(sample())
     total = time.perf_counter() - t0
-    n = rows * C5["ncol"]
     v = n * args.steps / sum(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "uniforms/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -364,10 +378,15 @@ def reference_arm(args, rank, world):
             "config": {"workload": "C5 runifGpu (bounded CPU sample: rows [0,2048) of the "
                                    "65536x65536 matrix on WorkGrid(1024,1024))",
                        "streams": C5["n_streams"]},
-            "cpu_baseline": {"value": v, "unit": "uniforms/s", "cores": orc.max_threads(),
-                             "kind": "port",
-                             "sample": f"{n} uniforms per step, oracle C port of "
-                                       "_kernels.fill_real (OpenMP, all host cores)"},
+            "cpu_baseline": {"value": v, "unit": "uniforms/s",
+                             "cores": int(os.environ.get("NUMBA_NUM_THREADS", os.cpu_count()))
+                             if kind == "reference" else orc.max_threads(),
+                             "kind": kind,
+                             "sample": f"{n} uniforms per step (rows [0,{rows}) of C5), "
+                                       + ("the unmodified reference's numba _kernels.fill_real "
+                                          "from baseline/_ref" if kind == "reference" else
+                                          "oracle C port of _kernels.fill_real (OpenMP)")
+                                       + ", all host cores"},
             "e2e": {"value": v, "unit": "uniforms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     try:
@@ -377,7 +396,90 @@ def reference_arm(args, rank, world):
         }
     except Exception as e:  # noqa: BLE001
         line["workloads"] = {"error": str(e)}
+    line["numba_reference"] = numba_reference(rows)
     print(json.dumps(line), flush=True)
+
+
+def _import_reference():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "streamforge")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/sfb_numba_cache")
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(os.cpu_count()))
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from streamforge import _kernels as K
+
+        return K
+    except Exception:
+        return None
+
+
+def numba_fill_sampler(rows):
+    """Callable timing one bounded C5 sample through the reference's own numba
+    kernel (baseline/_ref), or None when the reference is not installed."""
+    K = _import_reference()
+    if K is None:
+        return None
+    from oracle import oracle as orc
+
+    states, _ = orc.create_streams((12345,) * 6, C5["n_streams"])
+    out = np.zeros((rows, C5["ncol"]))
+    K.fill_real(states.copy(), out.ravel(), 64, C5["ncol"], C5["ncol"], C5["g0"], C5["g1"],
+                0, 1.0)  # JIT warm-up
+
+    def sample():
+        cur = states.copy()
+        t0 = time.perf_counter()
+        K.fill_real(cur, out.ravel(), rows, C5["ncol"], C5["ncol"], C5["g0"], C5["g1"], 0, 1.0)
+        return time.perf_counter() - t0
+
+    return sample
+
+
+def numba_reference(rows):
+    """The UNMODIFIED reference (streamforge, numba) from baseline/_ref, timed
+    through its own `_kernels` seam on the same bounded samples (informational
+    beside the oracle port; NUMBA_NUM_THREADS = all host cores)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "streamforge")):
+        return {"unavailable": "baseline/_ref not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/sfb_numba_cache")
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(os.cpu_count()))
+    sys.path.insert(0, ref)
+    try:
+        from scipy.special import gammaln
+        from streamforge import _kernels as K
+
+        from oracle import oracle as orc
+
+        states, _ = orc.create_streams((12345,) * 6, C5["n_streams"])
+        out = np.zeros((rows, C5["ncol"]))
+        K.fill_real(states.copy(), out.ravel(), 64, C5["ncol"], C5["ncol"], C5["g0"], C5["g1"],
+                    0, 1.0)  # JIT warm-up
+        best = None
+        for _ in range(3):
+            cur = states.copy()
+            t0 = time.perf_counter()
+            K.fill_real(cur, out.ravel(), rows, C5["ncol"], C5["ncol"], C5["g0"], C5["g1"], 0, 1.0)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        res = {"fill_uniform_per_s": rows * C5["ncol"] / best,
+               "threads": K.max_threads(), "sample": f"C5 rows [0,{rows}) via _kernels.fill_real"}
+        t = np.asarray(T4)
+        lf = gammaln(np.arange(t.sum() + 1, dtype=np.float64) + 1.0)
+        thr = float(-gammaln(t + 1.0).sum())
+        thr += 1e-7 * abs(thr)
+        st16, _ = orc.create_streams((12345,) * 6, 16384)
+        stats = np.empty(0)
+        K.fisher_replicates(st16.copy(), t.sum(1), t.sum(0), lf, thr, 1, 64, stats, False)
+        t0 = time.perf_counter()
+        K.fisher_replicates(st16.copy(), t.sum(1), t.sum(0), lf, thr, 62, 16384, stats, False)
+        res["fisher_T4_tables_per_s"] = 62 * 16384 / (time.perf_counter() - t0)
+        return res
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"{type(e).__name__}: {e}"}
 
 
 def _t10():
