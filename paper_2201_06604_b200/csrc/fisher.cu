@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "exp_glibc.cuh"
@@ -39,6 +41,7 @@ namespace sfb {
 constexpr int kMaxChunks = 96;
 constexpr int kFisherWalkDefault = 1;  // fisher_sampler.cuh walk form (tools/tune.py)
 constexpr int kFisherThreads = 256;
+constexpr int kMaxFisherSmem = 200 * 1024;
 
 struct ChunkJumps {
     Jump j[kMaxChunks];
@@ -166,35 +169,90 @@ static int check_margins(const int64_t *nrowt, int nr, const int64_t *ncolt, int
     return SFB_OK;
 }
 
-struct DeviceScratch {
-    void *p = nullptr;
-    cudaStream_t st = nullptr;
-    ~DeviceScratch() {
-        if (p) cudaFreeAsync(p, st);
+// Per-device cache of the kernel inputs (int32 margins + lf table).  The
+// reference recomputes nothing between replicates, and a fisher_sim call with
+// the same table re-uploads nothing here either: the packed bytes are compared
+// with the last upload and the device copy is reused.  New content goes through
+// a grow-only pinned staging buffer (truly async copy) into a grow-only device
+// buffer; before overwriting, the event recorded after the last kernel that
+// read the buffer is awaited.  The lock is held across the launch, so calls on
+// one device serialise their use of the buffer.
+struct InputCache {
+    std::mutex mu;
+    std::vector<unsigned char> key;
+    unsigned char *dev = nullptr, *pinned = nullptr;
+    size_t dev_cap = 0, pin_cap = 0;
+    cudaEvent_t last_use = nullptr;
+    bool pending = false;
+};
+
+static InputCache &input_cache() {
+    static InputCache caches[64];
+    int d = 0;
+    cudaGetDevice(&d);
+    return caches[d & 63];
+}
+
+struct StagedInputs {
+    std::unique_lock<std::mutex> lock;
+    InputCache *cache = nullptr;
+    int32_t *rowm = nullptr, *colm = nullptr;
+    double *lf = nullptr;
+    // record the consumer kernel (call after the launch)
+    void done(cudaStream_t st) {
+        if (cache->last_use == nullptr)
+            cudaEventCreateWithFlags(&cache->last_use, cudaEventDisableTiming);
+        cudaEventRecord(cache->last_use, st);
+        cache->pending = true;
     }
 };
 
-// stage margins (int32) and lf in one stream-ordered device allocation
 static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
-                        const double *lf, int64_t lf_len, cudaStream_t st, DeviceScratch &scr,
-                        int32_t **rowm, int32_t **colm, double **lfd) {
+                        const double *lf, int64_t lf_len, cudaStream_t st, StagedInputs &out) {
     const size_t lf_off = ((size_t)(nr + nc) * 4 + 15) & ~(size_t)15;
     const size_t bytes = lf_off + (size_t)lf_len * 8;
-    std::vector<unsigned char> host(bytes);
+    thread_local std::vector<unsigned char> host;
+    host.assign(bytes, 0);
     int32_t *hr = (int32_t *)host.data();
     for (int l = 0; l < nr; ++l) hr[l] = (int32_t)nrowt[l];
     for (int m = 0; m < nc; ++m) hr[nr + m] = (int32_t)ncolt[m];
     memcpy(host.data() + lf_off, lf, (size_t)lf_len * 8);
-    scr.st = st;
-    cudaError_t e = cudaMallocAsync(&scr.p, bytes, st);
-    if (e != cudaSuccess) return fail(SFB_E_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
-    e = cudaMemcpyAsync(scr.p, host.data(), bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return fail(SFB_E_CUDA, "margins upload: %s", cudaGetErrorString(e));
-    // pageable source: cudaMemcpyAsync returns once `host` has been copied to the
-    // driver's staging memory, so `host` may be freed on return (no sync needed)
-    *rowm = (int32_t *)scr.p;
-    *colm = *rowm + nr;
-    *lfd = (double *)((unsigned char *)scr.p + lf_off);
+    InputCache &c = input_cache();
+    out.lock = std::unique_lock<std::mutex>(c.mu);
+    out.cache = &c;
+    if (c.key != host) {
+        cudaError_t e = cudaSuccess;
+        if (c.pending) e = cudaEventSynchronize(c.last_use);  // previous readers done
+        if (e == cudaSuccess && bytes > c.dev_cap) {
+            if (c.dev) cudaFree(c.dev);
+            c.dev_cap = std::max(bytes, (size_t)1 << 20);
+            e = cudaMalloc((void **)&c.dev, c.dev_cap);
+        }
+        if (e == cudaSuccess && bytes > c.pin_cap) {
+            if (c.pinned) cudaFreeHost(c.pinned);
+            c.pin_cap = std::max(bytes, (size_t)1 << 20);
+            e = cudaMallocHost((void **)&c.pinned, c.pin_cap);
+        }
+        if (e == cudaSuccess) {
+            memcpy(c.pinned, host.data(), bytes);
+            e = cudaMemcpyAsync(c.dev, c.pinned, bytes, cudaMemcpyHostToDevice, st);
+        }
+        if (e == cudaSuccess && c.last_use == nullptr)
+            e = cudaEventCreateWithFlags(&c.last_use, cudaEventDisableTiming);
+        if (e == cudaSuccess) {  // the pinned buffer is busy until this copy lands
+            e = cudaEventRecord(c.last_use, st);
+            c.pending = true;
+        }
+        if (e != cudaSuccess) {
+            c.key.clear();
+            c.dev_cap = c.dev ? c.dev_cap : 0;
+            return fail(SFB_E_CUDA, "fisher input upload: %s", cudaGetErrorString(e));
+        }
+        c.key = host;
+    }
+    out.rowm = (int32_t *)c.dev;
+    out.colm = out.rowm + nr;
+    out.lf = (double *)(c.dev + lf_off);
     return SFB_OK;
 }
 
@@ -203,9 +261,18 @@ static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 template <bool LF_SMEM, int MINB, int WALK>
 static cudaError_t launch_fisher_walk(unsigned blocks, size_t smem, cudaStream_t st,
                                       const FisherArgs &a, const ChunkJumps &jumps) {
-    cudaError_t e = cudaFuncSetAttribute(fisher_kernel<LF_SMEM, MINB, WALK>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    // raise the dynamic shared-memory limit once per instantiation and device
+    static std::atomic<uint64_t> done_mask{0};
+    int d = 0;
+    cudaGetDevice(&d);
+    const uint64_t bit = 1ull << (d & 63);
+    if (!(done_mask.load() & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(fisher_kernel<LF_SMEM, MINB, WALK>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMaxFisherSmem);
+        if (e != cudaSuccess) return e;
+        done_mask.fetch_or(bit);
+    }
     fisher_kernel<LF_SMEM, MINB, WALK><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
     return cudaGetLastError();
 }
@@ -252,11 +319,10 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     }
     if (nloc == 0 || reps == 0) return SFB_OK;
 
-    DeviceScratch scr;
-    int32_t *rowm, *colm;
-    double *lfd;
-    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, scr, &rowm, &colm, &lfd))
-        return rc;
+    StagedInputs in;
+    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in)) return rc;
+    int32_t *rowm = in.rowm, *colm = in.colm;
+    double *lfd = in.lf;
 
     // chunking: enough units to fill the machine, bounded by kMaxChunks
     const int64_t F = (int64_t)(nr - 1) * (nc - 1);
@@ -298,7 +364,8 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     const bool lf_smem = head + lf_bytes + jw <= 110 * 1024;
     const size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
     const unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
-    if (smem > 200 * 1024) return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
+    if (smem > (size_t)kMaxFisherSmem)
+        return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
     // register cap: 4 CTAs/SM (64 regs) -- best for every table measured on
     // B200 (tools/tune.py sweep of 3 walk forms x {3, 4} CTAs/SM)
     const int minb = tune_knob("SFB_FISHER_MINB", 4);
@@ -319,6 +386,7 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher kernel launch: %s", cudaGetErrorString(e));
+    in.done(st);
     return SFB_OK;
 }
 
@@ -327,15 +395,13 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
     int ntot = 0;
     if (int rc = check_margins(nrowt, nr, ncolt, nc, lf, lf_len, &ntot)) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    DeviceScratch scr;
-    int32_t *rowm, *colm;
-    double *lfd;
-    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, scr, &rowm, &colm, &lfd))
-        return rc;
-    rcont2_kernel<<<1, 1, (size_t)std::max(nc, 1) * 4, st>>>(rowm, colm, nr, nc, ntot, lfd,
+    StagedInputs in;
+    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in)) return rc;
+    rcont2_kernel<<<1, 1, (size_t)std::max(nc, 1) * 4, st>>>(in.rowm, in.colm, nr, nc, ntot, in.lf,
                                                               d_state, d_mat);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "rcont2 launch: %s", cudaGetErrorString(e));
+    in.done(st);
     return SFB_OK;
 }
 

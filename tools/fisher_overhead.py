@@ -1,0 +1,55 @@
+"""Diagnose per-call overhead of the Fisher launch (T4, 1e6 tables)."""
+
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2201_06604_b200 as sf  # noqa: E402
+from paper_2201_06604_b200.fisher import launch_fisher, plan_fisher  # noqa: E402
+
+T4 = [[5, 9, 5, 7], [9, 5, 9, 7], [8, 6, 2, 6], [10, 8, 8, 8]]
+
+
+def main():
+    grid = sf.WorkGrid(256, 64)
+    st = sf.create_streams(sf.set_base_creator(), grid.size)[0]
+    plan = plan_fisher(np.asarray(T4), 10 ** 6, st, grid)
+    cur = st.device_current()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        launch_fisher(plan, cur, st.count, cnt)
+    torch.cuda.synchronize()
+    # (a) back to back
+    s.record()
+    for _ in range(10):
+        launch_fisher(plan, cur, st.count, cnt)
+    e.record()
+    e.synchronize()
+    print("back-to-back ms/launch", s.elapsed_time(e) / 10)
+    # (b) one at a time, synced, with and without flush
+    for flush in (False, True):
+        ts = []
+        for _ in range(10):
+            if flush:
+                scratch.zero_()
+            s.record()
+            t0 = time.perf_counter()
+            launch_fisher(plan, cur, st.count, cnt)
+            t1 = time.perf_counter()
+            e.record()
+            e.synchronize()
+            ts.append((s.elapsed_time(e), (t1 - t0) * 1e3))
+        print("flush" if flush else "noflush", "event ms / host launch ms:",
+              [f"{a:.3f}/{b:.3f}" for a, b in ts])
+
+
+if __name__ == "__main__":
+    main()
