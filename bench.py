@@ -546,9 +546,15 @@ def main():
         return reference_arm(args, rank, world)
     import torch
 
-    torch.cuda.set_device(local)
+    # SFB_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo -- a smoke test of
+    # the multi-rank path on a one-GPU box (numbers meaningless); default NCCL
+    share = os.environ.get("SFB_BENCH_SHARE_GPU") == "1"
+    torch.cuda.set_device(0 if share else local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2201_06604_b200 as sf
     from paper_2201_06604_b200 import _lib
 
