@@ -137,10 +137,6 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
 int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream);
 /* write-only HBM probe: fills `bytes` (multiple of 16) with 16-byte stores */
 int sfb_probe_write(void *d_out, int64_t bytes, void *stream);
-/* validation probe: the Fisher walk division (div_walk) vs IEEE __ddiv_rn on
- * 1184*256*per_thread pseudo-random walk operands; *d_bad += mismatches */
-int sfb_probe_div(uint64_t seed, int64_t per_thread, uint64_t *d_bad, double *d_example,
-                  void *stream);
 
 /* ---- test hooks (host execution of the device arithmetic) --------------- */
 /* runs the uint32 device step formulation on the host: n states x steps,

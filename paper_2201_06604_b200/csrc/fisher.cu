@@ -283,7 +283,6 @@ static cudaError_t launch_fisher(unsigned blocks, size_t smem, cudaStream_t st,
     switch (tune_knob("SFB_FISHER_WALK", kFisherWalkDefault)) {
         case 0: return launch_fisher_walk<LF_SMEM, MINB, 0>(blocks, smem, st, a, jumps);
         case 2: return launch_fisher_walk<LF_SMEM, MINB, 2>(blocks, smem, st, a, jumps);
-        case 3: return launch_fisher_walk<LF_SMEM, MINB, 3>(blocks, smem, st, a, jumps);
         default: return launch_fisher_walk<LF_SMEM, MINB, 1>(blocks, smem, st, a, jumps);
     }
 }

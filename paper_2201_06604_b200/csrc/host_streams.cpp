@@ -474,8 +474,6 @@ int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const
                                             LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
                 : walk == 2 ? sample_table<2>(rowm.data(), colm.data(), nr, nc, (int)ntot,
                                               LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
-                : walk == 3 ? sample_table<3>(rowm.data(), colm.data(), nr, nc, (int)ntot,
-                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
                             : sample_table<1>(rowm.data(), colm.data(), nr, nc, (int)ntot,
                                               LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr);
             hits += stat <= threshold;

@@ -71,7 +71,7 @@ def main():
                                   ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
                                   ("T10", t10, 1 << 23, (2048, 1024))):
             sim, fn = fisher_case(table, n, g)
-            for walk in (1, 3):
+            for walk in (0, 1, 2):
                 for mb in (3, 4):
                     os.environ["SFB_FISHER_MINB"] = str(mb)
                     os.environ["SFB_FISHER_WALK"] = str(walk)
