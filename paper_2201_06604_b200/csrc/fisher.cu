@@ -42,6 +42,8 @@ constexpr int kMaxChunks = 96;
 constexpr int kFisherWalkDefault = 1;  // fisher_sampler.cuh walk form (tools/tune.py)
 constexpr int kFisherThreads = 256;
 constexpr int kMaxFisherSmem = 200 * 1024;
+constexpr size_t kMaxMemo = 1 << 20;  // entries of the cell-(0,0) walk memo
+static const uint64_t kHostExpTab[256] = SFB_EXP_TABLE_INIT;
 
 struct ChunkJumps {
     Jump j[kMaxChunks];
@@ -58,6 +60,9 @@ struct FisherArgs {
     double threshold;
     int64_t item_lo, nloc, reps, rpc, nunits;
     int nr, nc, ntot, lf_len;
+    const double *memo_acc;  // memoised walk of cell (0,0) (nullable)
+    const int32_t *memo_k;
+    int memo_n, memo_tail, memo_forced, use_memo;
 };
 
 struct LfGlobal {
@@ -97,14 +102,16 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
             Mrg s = load_state(a.cur + 6 * w);
             if (c) apply(jumps.j[c], s);
             int *jw = jwork + threadIdx.x;
+            const WalkMemo memo{a.memo_acc, a.memo_k, a.memo_n, a.memo_tail, a.memo_forced};
+            const WalkMemo *mp = a.use_memo ? &memo : nullptr;
             for (int64_t rep = rep0; rep < rep1; ++rep) {
                 double stat;
                 if (LF_SMEM)
                     stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, LfShared{lfs}, exptab, s,
-                                        jw, blockDim.x, nullptr);
+                                        jw, blockDim.x, nullptr, mp);
                 else
                     stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, LfGlobal{a.lf}, exptab,
-                                        s, jw, blockDim.x, nullptr);
+                                        s, jw, blockDim.x, nullptr, mp);
                 if (stat <= a.threshold) ++hits;  // _kernels.py:275-276
                 if (a.stats) a.stats[local * a.reps + rep] = stat;
             }
@@ -198,6 +205,8 @@ struct StagedInputs {
     InputCache *cache = nullptr;
     int32_t *rowm = nullptr, *colm = nullptr;
     double *lf = nullptr;
+    double *memo_acc = nullptr;
+    int32_t *memo_k = nullptr;
     // record the consumer kernel (call after the launch)
     void done(cudaStream_t st) {
         if (cache->last_use == nullptr)
@@ -208,15 +217,24 @@ struct StagedInputs {
 };
 
 static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
-                        const double *lf, int64_t lf_len, cudaStream_t st, StagedInputs &out) {
+                        const double *lf, int64_t lf_len, cudaStream_t st, StagedInputs &out,
+                        const std::vector<double> *memo_acc = nullptr,
+                        const std::vector<int32_t> *memo_k = nullptr) {
     const size_t lf_off = ((size_t)(nr + nc) * 4 + 15) & ~(size_t)15;
-    const size_t bytes = lf_off + (size_t)lf_len * 8;
+    const size_t nm = memo_acc ? memo_acc->size() : 0;
+    const size_t macc_off = lf_off + (size_t)lf_len * 8;
+    const size_t mk_off = macc_off + nm * 8;
+    const size_t bytes = mk_off + nm * 4;
     thread_local std::vector<unsigned char> host;
     host.assign(bytes, 0);
     int32_t *hr = (int32_t *)host.data();
     for (int l = 0; l < nr; ++l) hr[l] = (int32_t)nrowt[l];
     for (int m = 0; m < nc; ++m) hr[nr + m] = (int32_t)ncolt[m];
     memcpy(host.data() + lf_off, lf, (size_t)lf_len * 8);
+    if (nm) {
+        memcpy(host.data() + macc_off, memo_acc->data(), nm * 8);
+        memcpy(host.data() + mk_off, memo_k->data(), nm * 4);
+    }
     InputCache &c = input_cache();
     out.lock = std::unique_lock<std::mutex>(c.mu);
     out.cache = &c;
@@ -253,6 +271,8 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
     out.rowm = (int32_t *)c.dev;
     out.colm = out.rowm + nr;
     out.lf = (double *)(c.dev + lf_off);
+    out.memo_acc = nm ? (double *)(c.dev + macc_off) : nullptr;
+    out.memo_k = nm ? (int32_t *)(c.dev + mk_off) : nullptr;
     return SFB_OK;
 }
 
@@ -319,8 +339,21 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     }
     if (nloc == 0 || reps == 0) return SFB_OK;
 
+    // memoised walk of cell (0,0): identical configuration in every replicate
+    thread_local std::vector<double> memo_acc;
+    thread_local std::vector<int32_t> memo_k;
+    int memo_tail = 0, memo_forced = 0;
+    const bool use_memo = nr >= 2 && nc >= 2 && tune_knob("SFB_FISHER_MEMO", 1) &&
+                          build_walk_memo((int)nrowt[0], (int)ncolt[0], ntot, LfPlain{lf},
+                                          kHostExpTab, kMaxMemo, memo_acc, memo_k, memo_tail,
+                                          memo_forced);
+    if (!use_memo) {
+        memo_acc.clear();
+        memo_k.clear();
+    }
     StagedInputs in;
-    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in)) return rc;
+    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in, &memo_acc, &memo_k))
+        return rc;
     int32_t *rowm = in.rowm, *colm = in.colm;
     double *lfd = in.lf;
 
@@ -357,6 +390,12 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     a.nc = nc;
     a.ntot = ntot;
     a.lf_len = (int)lf_len;
+    a.memo_acc = in.memo_acc;
+    a.memo_k = in.memo_k;
+    a.memo_n = (int)memo_acc.size();
+    a.memo_tail = memo_tail;
+    a.memo_forced = memo_forced;
+    a.use_memo = use_memo ? 1 : 0;
 
     const size_t head = 2048 + (size_t)(nr + nc) * 4 + 16;
     const size_t jw = (size_t)std::max(nc - 1, 1) * kFisherThreads * 4;

@@ -67,16 +67,18 @@ def main():
     if "fisher" in what:
         with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
             t10 = np.array(json.load(fh)["T10"])
+        month = np.loadtxt(os.path.join(ROOT, "tests", "golden", "month.csv"), delimiter=",") \
+            if os.path.exists(os.path.join(ROOT, "tests", "golden", "month.csv")) else None
         for name, table, n, g in (("T4", T4, 10 ** 6, (256, 64)),
                                   ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
                                   ("T10", t10, 1 << 23, (2048, 1024))):
             sim, fn = fisher_case(table, n, g)
-            for walk in (0, 1, 2):
+            for memo in (0, 1):
                 for mb in (3, 4):
                     os.environ["SFB_FISHER_MINB"] = str(mb)
-                    os.environ["SFB_FISHER_WALK"] = str(walk)
+                    os.environ["SFB_FISHER_MEMO"] = str(memo)
                     ms = timeit(fn, reps=3, warm=1)
-                    res.append({"w": f"fisher_{name}", "variant": f"walk{walk}_minb{mb}",
+                    res.append({"w": f"fisher_{name}", "variant": f"memo{memo}_minb{mb}",
                                 "ms": ms, "per_s": sim / (ms / 1e3)})
                     print(json.dumps(res[-1]), flush=True)
 
