@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -42,7 +43,6 @@ constexpr int kMaxChunks = 96;
 constexpr int kFisherWalkDefault = 1;  // fisher_sampler.cuh walk form (tools/tune.py)
 constexpr int kFisherThreads = 256;
 constexpr int kMaxFisherSmem = 200 * 1024;
-constexpr size_t kMaxMemo = 1 << 20;  // entries of the cell-(0,0) walk memo
 static const uint64_t kHostExpTab[256] = SFB_EXP_TABLE_INIT;
 
 struct ChunkJumps {
@@ -60,9 +60,8 @@ struct FisherArgs {
     double threshold;
     int64_t item_lo, nloc, reps, rpc, nunits;
     int nr, nc, ntot, lf_len;
-    const double *memo_acc;  // memoised walk of cell (0,0) (nullable)
-    const int32_t *memo_k;
-    int memo_n, memo_tail, memo_forced, use_memo;
+    MemoSet memo;  // memoised first-row / first-column walks
+    int use_memo;
 };
 
 struct LfGlobal {
@@ -102,8 +101,8 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
             Mrg s = load_state(a.cur + 6 * w);
             if (c) apply(jumps.j[c], s);
             int *jw = jwork + threadIdx.x;
-            const WalkMemo memo{a.memo_acc, a.memo_k, a.memo_n, a.memo_tail, a.memo_forced};
-            const WalkMemo *mp = a.use_memo ? &memo : nullptr;
+            const MemoSet memo = a.memo;
+            const MemoSet *mp = a.use_memo ? &memo : nullptr;
             for (int64_t rep = rep0; rep < rep1; ++rep) {
                 double stat;
                 if (LF_SMEM)
@@ -187,6 +186,7 @@ static int check_margins(const int64_t *nrowt, int nr, const int64_t *ncolt, int
 struct InputCache {
     std::mutex mu;
     std::vector<unsigned char> key;
+    uint64_t memo_version = 0;
     unsigned char *dev = nullptr, *pinned = nullptr;
     size_t dev_cap = 0, pin_cap = 0;
     cudaEvent_t last_use = nullptr;
@@ -205,8 +205,7 @@ struct StagedInputs {
     InputCache *cache = nullptr;
     int32_t *rowm = nullptr, *colm = nullptr;
     double *lf = nullptr;
-    double *memo_acc = nullptr;
-    int32_t *memo_k = nullptr;
+    MemoSet memo{};
     // record the consumer kernel (call after the launch)
     void done(cudaStream_t st) {
         if (cache->last_use == nullptr)
@@ -216,29 +215,35 @@ struct StagedInputs {
     }
 };
 
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Upload (or reuse) [margins | lf | memo tables] for this call.  The cache key
+// is the packed margins + lf bytes plus the memo version (memo tables are a
+// deterministic function of them).
 static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
                         const double *lf, int64_t lf_len, cudaStream_t st, StagedInputs &out,
-                        const std::vector<double> *memo_acc = nullptr,
-                        const std::vector<int32_t> *memo_k = nullptr) {
-    const size_t lf_off = ((size_t)(nr + nc) * 4 + 15) & ~(size_t)15;
-    const size_t nm = memo_acc ? memo_acc->size() : 0;
-    const size_t macc_off = lf_off + (size_t)lf_len * 8;
-    const size_t mk_off = macc_off + nm * 8;
-    const size_t bytes = mk_off + nm * 4;
+                        const HostMemo *hm = nullptr, uint64_t memo_version = 0) {
+    const size_t lf_off = align16((size_t)(nr + nc) * 4);
+    const size_t key_bytes = lf_off + (size_t)lf_len * 8;
+    size_t row_off = align16(key_bytes), col_off = row_off, cfg_off = row_off,
+           acc_off = row_off, k_off = row_off, bytes = key_bytes;
+    if (hm) {
+        col_off = align16(row_off + hm->row.size() * sizeof(MemoCellDesc));
+        cfg_off = align16(col_off + hm->col.size() * sizeof(MemoCellDesc));
+        acc_off = align16(cfg_off + hm->cfg.size() * sizeof(MemoConfig));
+        k_off = align16(acc_off + hm->acc.size() * 8);
+        bytes = k_off + hm->k.size() * 4;
+    }
     thread_local std::vector<unsigned char> host;
-    host.assign(bytes, 0);
+    host.assign(key_bytes, 0);
     int32_t *hr = (int32_t *)host.data();
     for (int l = 0; l < nr; ++l) hr[l] = (int32_t)nrowt[l];
     for (int m = 0; m < nc; ++m) hr[nr + m] = (int32_t)ncolt[m];
     memcpy(host.data() + lf_off, lf, (size_t)lf_len * 8);
-    if (nm) {
-        memcpy(host.data() + macc_off, memo_acc->data(), nm * 8);
-        memcpy(host.data() + mk_off, memo_k->data(), nm * 4);
-    }
     InputCache &c = input_cache();
     out.lock = std::unique_lock<std::mutex>(c.mu);
     out.cache = &c;
-    if (c.key != host) {
+    if (c.key != host || c.memo_version != memo_version) {
         cudaError_t e = cudaSuccess;
         if (c.pending) e = cudaEventSynchronize(c.last_use);  // previous readers done
         if (e == cudaSuccess && bytes > c.dev_cap) {
@@ -252,7 +257,14 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
             e = cudaMallocHost((void **)&c.pinned, c.pin_cap);
         }
         if (e == cudaSuccess) {
-            memcpy(c.pinned, host.data(), bytes);
+            memcpy(c.pinned, host.data(), key_bytes);
+            if (hm) {
+                memcpy(c.pinned + row_off, hm->row.data(), hm->row.size() * sizeof(MemoCellDesc));
+                memcpy(c.pinned + col_off, hm->col.data(), hm->col.size() * sizeof(MemoCellDesc));
+                memcpy(c.pinned + cfg_off, hm->cfg.data(), hm->cfg.size() * sizeof(MemoConfig));
+                memcpy(c.pinned + acc_off, hm->acc.data(), hm->acc.size() * 8);
+                memcpy(c.pinned + k_off, hm->k.data(), hm->k.size() * 4);
+            }
             e = cudaMemcpyAsync(c.dev, c.pinned, bytes, cudaMemcpyHostToDevice, st);
         }
         if (e == cudaSuccess && c.last_use == nullptr)
@@ -267,13 +279,50 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
             return fail(SFB_E_CUDA, "fisher input upload: %s", cudaGetErrorString(e));
         }
         c.key = host;
+        c.memo_version = memo_version;
     }
     out.rowm = (int32_t *)c.dev;
     out.colm = out.rowm + nr;
     out.lf = (double *)(c.dev + lf_off);
-    out.memo_acc = nm ? (double *)(c.dev + macc_off) : nullptr;
-    out.memo_k = nm ? (int32_t *)(c.dev + mk_off) : nullptr;
+    if (hm)
+        out.memo = MemoSet{(const MemoCellDesc *)(c.dev + row_off),
+                           (const MemoCellDesc *)(c.dev + col_off),
+                           (const MemoConfig *)(c.dev + cfg_off), (const double *)(c.dev + acc_off),
+                           (const int32_t *)(c.dev + k_off)};
     return SFB_OK;
+}
+
+// Process-wide cache of the memo tables of the last table seen (building them
+// walks every tabulated configuration once on the host: tens of ms for T10).
+struct MemoCache {
+    std::mutex mu;
+    std::vector<int64_t> margins;
+    std::vector<double> lf;
+    std::shared_ptr<const HostMemo> memo;
+    uint64_t version = 0;
+};
+
+static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, const int64_t *ncolt,
+                                                int nc, int ntot, const double *lf, int64_t lf_len,
+                                                uint64_t *version) {
+    static MemoCache mc;
+    std::lock_guard<std::mutex> g(mc.mu);
+    std::vector<int64_t> key(nrowt, nrowt + nr);
+    key.push_back(-1);
+    key.insert(key.end(), ncolt, ncolt + nc);
+    if (!mc.memo || key != mc.margins || (int64_t)mc.lf.size() != lf_len ||
+        memcmp(mc.lf.data(), lf, (size_t)lf_len * 8) != 0) {
+        std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
+        auto hm = std::make_shared<HostMemo>();
+        build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
+                       kMemoMaxEntries, kMemoMaxSeq, kMemoSigmas);
+        mc.memo = hm;
+        mc.margins = key;
+        mc.lf.assign(lf, lf + lf_len);
+        ++mc.version;
+    }
+    *version = mc.version;
+    return mc.memo;
 }
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -339,20 +388,13 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     }
     if (nloc == 0 || reps == 0) return SFB_OK;
 
-    // memoised walk of cell (0,0): identical configuration in every replicate
-    thread_local std::vector<double> memo_acc;
-    thread_local std::vector<int32_t> memo_k;
-    int memo_tail = 0, memo_forced = 0;
-    const bool use_memo = nr >= 2 && nc >= 2 && tune_knob("SFB_FISHER_MEMO", 1) &&
-                          build_walk_memo((int)nrowt[0], (int)ncolt[0], ntot, LfPlain{lf},
-                                          kHostExpTab, kMaxMemo, memo_acc, memo_k, memo_tail,
-                                          memo_forced);
-    if (!use_memo) {
-        memo_acc.clear();
-        memo_k.clear();
-    }
+    // memoised first-row / first-column walks (cached per table)
+    const bool use_memo = nr >= 2 && nc >= 2 && tune_knob("SFB_FISHER_MEMO", 1);
+    uint64_t memo_version = 0;
+    std::shared_ptr<const HostMemo> hm;
+    if (use_memo) hm = get_memo(nrowt, nr, ncolt, nc, ntot, lf, lf_len, &memo_version);
     StagedInputs in;
-    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in, &memo_acc, &memo_k))
+    if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in, hm.get(), memo_version))
         return rc;
     int32_t *rowm = in.rowm, *colm = in.colm;
     double *lfd = in.lf;
@@ -390,11 +432,7 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     a.nc = nc;
     a.ntot = ntot;
     a.lf_len = (int)lf_len;
-    a.memo_acc = in.memo_acc;
-    a.memo_k = in.memo_k;
-    a.memo_n = (int)memo_acc.size();
-    a.memo_tail = memo_tail;
-    a.memo_forced = memo_forced;
+    a.memo = in.memo;
     a.use_memo = use_memo ? 1 : 0;
 
     const size_t head = 2048 + (size_t)(nr + nc) * 4 + 16;

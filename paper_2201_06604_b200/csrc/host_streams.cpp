@@ -464,18 +464,25 @@ int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const
     std::vector<int> jw(nc > 1 ? nc - 1 : 1);
     int64_t ntot = 0;
     for (int l = 0; l < nr; ++l) ntot += nrowt[l];
+    HostMemo hm;
+    const bool use_memo = tune_knob("SFB_FISHER_MEMO", 1) != 0;
+    if (use_memo)
+        build_memo_set(rowm.data(), nr, colm.data(), nc, (int)ntot, LfPlain{lf}, kExpTable, hm,
+                       kMemoMaxEntries, kMemoMaxSeq, kMemoSigmas);
+    const MemoSet ms = hm.view();
+    const MemoSet *mp = use_memo ? &ms : nullptr;
+    const int walk = tune_knob("SFB_FISHER_WALK", 1);
     int64_t hits = 0;
     for (int64_t w = item_lo; w < item_hi; ++w) {
         Mrg s = load_state(cur + 6 * w);
         for (int64_t rep = 0; rep < reps; ++rep) {
-            const int walk = tune_knob("SFB_FISHER_WALK", 1);
             const double stat =
                 walk == 0 ? sample_table<0>(rowm.data(), colm.data(), nr, nc, (int)ntot,
-                                            LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
+                                            LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp)
                 : walk == 2 ? sample_table<2>(rowm.data(), colm.data(), nr, nc, (int)ntot,
-                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr)
+                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp)
                             : sample_table<1>(rowm.data(), colm.data(), nr, nc, (int)ntot,
-                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr);
+                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp);
             hits += stat <= threshold;
             if (stats) stats[(w - item_lo) * reps + rep] = stat;
         }
