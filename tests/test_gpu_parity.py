@@ -487,3 +487,37 @@ def test_fisher_walk_forms_bit_exact(G, A, walk, monkeypatch):
         assert sha(st.current) == g["states_sha"]
         if want:
             assert np.array_equal(r.statistics, A[key + "_stats"])
+
+
+@pytest.mark.slow
+def test_fisher_c4_full_scale_sampled_items(G):
+    # C4 (BASELINE configs[3]): T10, 1e10 tables on grid (2048, 1024), 2^21
+    # streams (4769 reps per item).  The total count is checked for
+    # consistency with the per-item counts; 256 random items are re-run on the
+    # oracle (1.2e6 tables) and must match counts and final states bit for bit.
+    import torch
+
+    from paper_2201_06604_b200.fisher import launch_fisher, plan_fisher
+
+    t10 = np.array(G["T10"])
+    grid = sf.WorkGrid(2048, 1024)
+    st = fresh(grid.size)
+    plan = plan_fisher(t10, 10 ** 10, st, grid)
+    assert plan.reps == 4769 and plan.sim_num == 10001317888
+    cur = st.device_current()
+    ic = torch.zeros(grid.size, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    launch_fisher(plan, cur, st.count, cnt, item_counts_dev=ic)
+    st._mark_device_ahead()
+    ic = ic.cpu().numpy()
+    assert ic.sum() == int(cnt.item())
+    rng = np.random.default_rng(2201)
+    items = rng.choice(grid.size, 256, replace=False)
+    ref_st = oa.fresh_states(grid.size)
+    final = st.current
+    for w in items:
+        one = np.zeros(1, np.int64)
+        orc.fisher_replicates(ref_st, t10.sum(1), t10.sum(0), plan.lf, plan.kernel_threshold,
+                              plan.reps, int(w) + 1, item_lo=int(w), item_counts=one)
+        assert ic[w] == one[0], w
+        assert np.array_equal(final[w], ref_st[w]), w
