@@ -432,3 +432,14 @@ def test_device_fisher_sampler_edge_tables(A, key):
     t = A["tab_" + key[2:]]
     cnt, rcnt, cur, ref, st, rst = _host_fisher(t, 0, 16, reps_override=200, stats=True)
     assert cnt == rcnt and np.array_equal(cur, ref) and np.array_equal(st, rst)
+
+
+def test_device_fisher_sampler_large_margins():
+    # margins ~1e6: memo tables hit their budgets / skip rules; results exact
+    import time
+
+    t = np.array([[300000, 200000, 150000], [250000, 250000, 1000], [7, 70000, 30000]])
+    t0 = time.time()
+    cnt, rcnt, cur, ref, st, rst = _host_fisher(t, 0, 8, reps_override=3, stats=True)
+    assert time.time() - t0 < 60
+    assert cnt == rcnt and np.array_equal(cur, ref) and np.array_equal(st, rst)
