@@ -493,19 +493,27 @@ def _t10():
 
 def run_probes(torch, _lib):
     """Roofline denominators MEASURED_PEAKS.json lacks: write-only HBM
-    bandwidth (sfb_probe_write: 16-byte streaming stores over 16 GiB) and the FP64 pipe (sfb_probe_fp64:
+    bandwidth (sfb_probe_write: 16-byte streaming stores over 16 GiB, best of a
+    grid-stride sweep and per-CTA contiguous segments) and the FP64 pipe (sfb_probe_fp64:
     8 independent DFMA chains per thread, 8 CTAs of 256 per SM)."""
     out = {}
     buf = torch.empty(16 << 30, dtype=torch.uint8, device="cuda")
     tm = Timer(torch)
     best = None
     st = _lib.stream_handle()
-    for _ in range(4):
-        tm.start()
-        _lib.check(_lib.lib().sfb_probe_write(_lib.dptr(buf), buf.numel(), st))
-        ms = tm.stop()
-        best = ms if best is None else min(best, ms)
+    per_variant = {}
+    for variant in (0, 1):
+        vbest = None
+        for _ in range(4):
+            tm.start()
+            _lib.check(_lib.lib().sfb_probe_write(_lib.dptr(buf), buf.numel(), variant, st))
+            ms = tm.stop()
+            vbest = ms if vbest is None else min(vbest, ms)
+        per_variant[variant] = buf.numel() / (vbest / 1e3) / 1e9
+        best = vbest if best is None else min(best, vbest)
     out["hbm_write_gbs"] = buf.numel() / (best / 1e3) / 1e9
+    out["hbm_write_gbs_by_shape"] = {"grid_stride": per_variant[0],
+                                     "cta_segments": per_variant[1]}
     del buf
     d = torch.zeros(1, dtype=torch.float64, device="cuda")
     blocks, iters = 148 * 8, 4096

@@ -135,8 +135,9 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
 /* ---- measurement ---------------------------------------------------------- */
 /* FP64-pipe roofline probe (bench.py): blocks x 256 threads x iters x 8 DFMA */
 int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream);
-/* write-only HBM probe: fills `bytes` (multiple of 16) with 16-byte stores */
-int sfb_probe_write(void *d_out, int64_t bytes, void *stream);
+/* write-only HBM probe: fills `bytes` (multiple of 16) with 16-byte stores;
+ * variant 0 = grid-stride sweep, 1 = per-CTA contiguous segments (fill shape) */
+int sfb_probe_write(void *d_out, int64_t bytes, int variant, void *stream);
 
 /* ---- test hooks (host execution of the device arithmetic) --------------- */
 /* runs the uint32 device step formulation on the host: n states x steps,

@@ -25,7 +25,11 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double *out, int iters,
     if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
-// write-only HBM probe: 16-byte streaming stores, grid-stride
+// write-only HBM probes, 16-byte streaming stores.
+//   variant 0: grid-stride (the whole grid sweeps the buffer front to back);
+//   variant 1: each CTA owns a contiguous segment and writes it with 4
+//              independent stores in flight per thread -- the access shape of
+//              fill_uniform_fast (many warps writing far-apart 512-byte runs).
 __global__ void __launch_bounds__(256) write_probe_kernel(double2 *out, int64_t n) {
     const double2 v = make_double2(1.0, 2.0);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -33,12 +37,34 @@ __global__ void __launch_bounds__(256) write_probe_kernel(double2 *out, int64_t 
         __stcs(out + i, v);
 }
 
+__global__ void __launch_bounds__(256) write_probe_seg_kernel(double2 *out, int64_t n,
+                                                              int64_t seg) {
+    const double2 v = make_double2(1.0, 2.0);
+    const int64_t b0 = (int64_t)blockIdx.x * seg, b1 = min(b0 + seg, n);
+    int64_t i = b0 + threadIdx.x;
+    for (; i + 3 * 256 < b1; i += 4 * 256) {
+        __stcs(out + i, v);
+        __stcs(out + i + 256, v);
+        __stcs(out + i + 512, v);
+        __stcs(out + i + 768, v);
+    }
+    for (; i < b1; i += 256) __stcs(out + i, v);
+}
+
 }  // namespace sfb
 
 using namespace sfb;
 
-extern "C" int sfb_probe_write(void *d_out, int64_t bytes, void *stream) {
-    write_probe_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>((double2 *)d_out, bytes / 16);
+extern "C" int sfb_probe_write(void *d_out, int64_t bytes, int variant, void *stream) {
+    const int64_t n = bytes / 16;
+    if (variant == 1) {
+        const int64_t blocks = 148 * 64;
+        const int64_t seg = (n + blocks - 1) / blocks;
+        write_probe_seg_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+            (double2 *)d_out, n, seg);
+    } else {
+        write_probe_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>((double2 *)d_out, n);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "write probe: %s", cudaGetErrorString(e));
     return SFB_OK;

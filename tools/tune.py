@@ -1,4 +1,4 @@
-"""Kernel-variant sweep (tuning knobs SFB_NORMAL_VARIANT / SFB_FISHER_MINB).
+"""Kernel-variant sweep (tuning knobs SFB_NORMAL_VARIANT, SFB_FISHER_WALK/MINB).
 
     python tools/tune.py [normal] [fisher]
 
@@ -48,7 +48,13 @@ def fisher_case(table, n, g):
     plan = plan_fisher(np.asarray(table), n, st, grid)
     cur = st.device_current()
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    return plan.sim_num, lambda: launch_fisher(plan, cur, st.count, cnt)
+    cur0 = cur.clone()
+
+    def run():
+        cur.copy_(cur0)  # same input states every launch (counts comparable)
+        launch_fisher(plan, cur, st.count, cnt)
+
+    return plan.sim_num, run, cnt
 
 
 def main():
@@ -69,19 +75,24 @@ def main():
             t10 = np.array(json.load(fh)["T10"])
         month = np.loadtxt(os.path.join(ROOT, "tests", "golden", "month.csv"), delimiter=",") \
             if os.path.exists(os.path.join(ROOT, "tests", "golden", "month.csv")) else None
+        only = os.environ.get("TUNE_FISHER_TABLES", "T4,T4x16,T10").split(",")
+        walks = os.environ.get("TUNE_FISHER_WALKS", "1,3").split(",")
         for name, table, n, g in (("T4", T4, 10 ** 6, (256, 64)),
                                   ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
                                   ("T10", t10, 1 << 23, (2048, 1024))):
-            sim, fn = fisher_case(table, n, g)
-            for memo in (0, 1):
+            if name not in only:
+                continue
+            sim, fn, cnt = fisher_case(table, n, g)
+            for walk in walks:
                 for mb in (3, 4):
                     os.environ["SFB_FISHER_MINB"] = str(mb)
-                    os.environ["SFB_FISHER_MEMO"] = str(memo)
+                    os.environ["SFB_FISHER_WALK"] = walk
                     ms = timeit(fn, reps=3, warm=1)
-                    res.append({"w": f"fisher_{name}", "variant": f"memo{memo}_minb{mb}",
-                                "ms": ms, "per_s": sim / (ms / 1e3)})
+                    fn()
+                    res.append({"w": f"fisher_{name}", "variant": f"walk{walk}_minb{mb}",
+                                "ms": ms, "per_s": sim / (ms / 1e3),
+                                "count_one_launch": int(cnt.item())})
                     print(json.dumps(res[-1]), flush=True)
-
 
 if __name__ == "__main__":
     main()
