@@ -133,6 +133,9 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
                      int64_t *d_mat, void *stream);
 
 /* ---- measurement ---------------------------------------------------------- */
+/* the rsqrt.approx.f64 seed used by the float32 Box-Muller form, elementwise
+ * (accuracy test, tests/test_gpu_parity.py) */
+int sfb_probe_rsqrt(const double *d_x, double *d_y, int64_t n, void *stream);
 /* FP64-pipe roofline probe (bench.py): blocks x 256 threads x iters x 8 DFMA */
 int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream);
 /* write-only HBM probe: fills `bytes` (multiple of 16) with 16-byte stores;
@@ -154,6 +157,11 @@ int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double 
 /* the device Fisher sampler (fisher_sampler.cuh) run serially on the host over
  * items [item_lo, item_hi) (states int64 (n,6), mutated; stats nullable,
  * indexed (w - item_lo)*reps + rep; *count = hits) -- CPU test hook */
+/* test hook: the float32 Box-Muller form (box_muller_pair_f32) on the host,
+ * with `newton` sqrt corrections and a modelled rsqrt seed of relative error
+ * seed_rel_err */
+int sfb_host_box_muller_f32(const int64_t *z1, const int64_t *z2, int64_t n, int newton,
+                            double seed_rel_err, float *a, float *b);
 int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr,
                                const int64_t *ncolt, int nc, const double *lf,
                                double threshold, int64_t reps, int64_t item_lo,

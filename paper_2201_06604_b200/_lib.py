@@ -31,6 +31,7 @@ _ERRORS = {
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _f64p = ctypes.POINTER(ctypes.c_double)
+_f32p = ctypes.POINTER(ctypes.c_float)
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
@@ -61,11 +62,13 @@ _SIGS = {
                               _int),
     "sfb_rcont2_table": ([_i64p, _int, _i64p, _int, _f64p, _i64, _vp, _vp, _vp], _int),
     "sfb_probe_fp64": ([_vp, _i64, _int, _vp], _int),
+    "sfb_probe_rsqrt": ([_vp, _vp, _i64, _vp], _int),
     "sfb_probe_write": ([_vp, _i64, _int, _vp], _int),
     "sfb_host_step_u32": ([_i64p, _i64, _i64, _i64p], _int),
     "sfb_host_exp": ([ctypes.c_double], ctypes.c_double),
     "sfb_host_log1p": ([ctypes.c_double], ctypes.c_double),
     "sfb_host_box_muller": ([_i64p, _i64p, _i64, _f64p, _f64p], _int),
+    "sfb_host_box_muller_f32": ([_i64p, _i64p, _i64, _int, ctypes.c_double, _f32p, _f32p], _int),
     "sfb_host_fisher_replicates": ([_i64p, _i64p, _int, _i64p, _int, _f64p, ctypes.c_double,
                                     _i64, _i64, _i64, _f64p, _i64p], _int),
 }

@@ -42,7 +42,7 @@ namespace sfb {
 enum BmCoef {
     kC_Ln2Hi, kC_Ln2Lo, kC_L5, kC_L4, kC_L3, kC_L2,  // ln(1+r) coefficients 1/5, -1/4, 1/3, -1/2
     kC_S5, kC_S3, kC_C4, kC_C2,                      // sin B, cos B - 1
-    kC_TwoPiNorm, kC_HalfPi, kC_PiO2Lo, kC_Neg2, kC_Count
+    kC_TwoPiNorm, kC_HalfPi, kC_PiO2Lo, kC_Neg2, kC_Ln2, kC_Half, kC_Count
 };
 
 #define SFB_BM_COEF_INIT                                                                 \
@@ -53,7 +53,7 @@ enum BmCoef {
             1.0 / 24.0, -1.0 / 2.0, (2.0 * 3.141592653589793) / 2147483648.0,            \
             0.5 * 3.141592653589793, /* HALFPI, _kernels.py:22 */                         \
             6.123233995736766e-17,   /* pi/2 - HALFPI */                                  \
-            -2.0                                                                         \
+            -2.0, 6.93147180559945286227e-01, /* ln 2 rounded */ 0.5                     \
     }
 
 #ifdef __CUDACC__
@@ -129,6 +129,128 @@ SFB_EXP_HD void box_muller_pair(uint32_t z1m1, uint32_t z2m1, const uint64_t *lo
     const double d = rounding_error_minus_halfpi(theta, thb) + SFB_BMC(kC_PiO2Lo);
     a = radius * cos_t;
     b = radius * fma_rn(d, cos_t, sin_t);
+}
+
+// ---------------------------------------------------------------------------
+// Float32-output form (rnormGpu with float32 output -- an extension; the
+// reference is float64-only, and float32(reference) is the target).  Each
+// output is rounded to float32 once, so the transform needs a relative error
+// far below 2^-24, not the ~2^-52 of box_muller_pair: this form targets
+// <= 2^-44, so a result can differ from float32(reference) only when the
+// reference lies within ~2^-44 of a float32 rounding boundary (expected rate
+// ~1e-6 of cells, by 1 ulp_f32).  FP64 work drops from ~45 to ~25 ops/pair:
+//   * log: k ln2 + ln c in one fma against a table of (1/c, ln c rounded)
+//     pairs (one 16-byte load), degree-5 polynomial kept (|r| <= 2^-10 and
+//     ln u1 ~ r near u1 = 1, where r^5/5 is 2^-42 relative);
+//   * sqrt: rsqrt.approx seed (MUFU.RSQ64H, measured <= 2^-20.06 relative on
+//     B200), one Newton step on 1/sqrt and one residual-corrected step on
+//     sqrt (NEWTON = 2; error ~(1.5 e^2)^2, far below 2^-53);
+//   * trig: sin B to B^3 (B^5/120 < 2.3e-15 absolute), cos B - 1 to B^4,
+//     fused fma recombination; (cos A, sin A) as one 16-byte load;
+//   * lane b = R sin(theta): the reference's cos(fl(theta - fl(pi/2))) differs
+//     by d cos(theta), |d| <= 2^-53 pi, which is below the float32 resolution
+//     except where sin(theta) itself is tiny: z2 within kBmExactWin of a
+//     multiple of 2^30 (theta near 0, pi, 2 pi).  Those pairs (~1e-5 of all)
+//     take the full-accuracy box_muller_pair (tables in global memory).
+//   Near the zeros of cos and sin elsewhere the table points A_k sit exactly
+//   on the reference's fl(k pi/2), so cos_t / sin_t stay relatively accurate.
+struct alignas(16) BmPair {
+    double x, y;
+};
+constexpr int kBmFastLogPairs = SFB_BM_LOG_N;         // (1/c, ln c)
+constexpr int kBmFastTrigPairs = SFB_BM_TRIG_N + 1;   // (cos A, sin A)
+
+// fill the fast-path tables from the table words of bm_tables.inc
+SFB_EXP_HD void bm_fast_tables(const uint64_t *logw, const uint64_t *trigw, int t, int nt,
+                               BmPair *logp, BmPair *trigp, double *angle) {
+    for (int i = t; i < kBmFastLogPairs; i += nt)
+        logp[i] = BmPair{as_f64(logw[3 * i]), as_f64(logw[3 * i + 1]) + as_f64(logw[3 * i + 2])};
+    for (int i = t; i < kBmFastTrigPairs; i += nt) {
+        trigp[i] = BmPair{as_f64(trigw[3 * i + 1]), as_f64(trigw[3 * i + 2])};
+        angle[i] = as_f64(trigw[3 * i]);
+    }
+}
+
+// 1/sqrt(x) seeds: the hardware approximation (MUFU.RSQ64H) on the device;
+// on the host a model with a chosen relative error (CPU tests use the bound
+// measured on the B200, tests/test_gpu_parity.py::test_rsqrt_seed_accuracy)
+struct RsqrtSeedHw {
+    SFB_EXP_HD double operator()(double x) const {
+#ifdef __CUDA_ARCH__
+        double y;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+        return y;
+#else
+        return 1.0 / sqrt(x);
+#endif
+    }
+};
+struct RsqrtSeedModel {
+    double rel_err;  // the seed is RN(1/sqrt(x)) * (1 + rel_err)
+    SFB_EXP_HD double operator()(double x) const { return (1.0 / sqrt(x)) * (1.0 + rel_err); }
+};
+
+constexpr uint32_t kBmExactWin = 1u << 12;
+
+#ifdef __CUDACC__
+#define SFB_BM_COLD static __host__ __device__ __noinline__
+#else
+#define SFB_BM_COLD inline
+#endif
+// the rare exact path, kept out of line so the hot loop stays compact
+struct F32Pair {
+    float a, b;
+};
+SFB_BM_COLD F32Pair box_muller_pair_f32_exact(uint32_t z1m1, uint32_t z2m1,
+                                              const uint64_t *logw, const uint64_t *trigw) {
+    double da, db;
+    box_muller_pair(z1m1, z2m1, logw, trigw, da, db);
+    return F32Pair{(float)da, (float)db};
+}
+
+template <int NEWTON, typename SEED = RsqrtSeedHw>
+SFB_EXP_HD void box_muller_pair_f32(uint32_t z1m1, uint32_t z2m1, const BmPair *logp,
+                                    const BmPair *trigp, const double *angle,
+                                    const uint64_t *logw, const uint64_t *trigw, float &a,
+                                    float &b, const SEED &seed = SEED()) {
+    if (((z2m1 + 1u + kBmExactWin) & ((1u << 30) - 1u)) < 2u * kBmExactWin) {
+        const F32Pair p = box_muller_pair_f32_exact(z1m1, z2m1, logw, trigw);  // theta ~ 0, pi, 2pi
+        a = p.a;
+        b = p.b;
+        return;
+    }
+    const double d = (double)(z1m1 + 1u);  // exact
+    const uint64_t bits = as_u64(d);
+    const int k = (int)(bits >> 52) - 1053;
+    const double m = as_f64((bits & 0x000fffffffffffffull) | 0x3fe0000000000000ull);
+    const BmPair lc = logp[(uint32_t)(bits >> 43) & (SFB_BM_LOG_N - 1)];
+    const double r = fma_rn(m, lc.x, -1.0);
+    double p = fma_rn(r, SFB_BMC(kC_L5), SFB_BMC(kC_L4));
+    p = fma_rn(r, p, SFB_BMC(kC_L3));
+    p = fma_rn(r, p, SFB_BMC(kC_L2));
+    const double r2 = r * r;
+    const double y = fma_rn((double)k, SFB_BMC(kC_Ln2), lc.y);
+    const double x = SFB_BMC(kC_Neg2) * (y + fma_rn(r2, p, r));  // -2 ln u1 (scaling exact)
+    double yr = seed(x);
+    if (NEWTON >= 2) {  // y <- y + y/2 (1 - x y^2)
+        const double e = fma_rn(-x, yr * yr, 1.0);
+        yr = fma_rn(SFB_BMC(kC_Half) * yr, e, yr);
+    }
+    const double s0 = x * yr;
+    const double R = fma_rn(fma_rn(-s0, s0, x), SFB_BMC(kC_Half) * yr, s0);
+    // theta = fl((2 pi NORM) z2) exactly as the reference rounds it
+    const double c = SFB_BMC(kC_TwoPiNorm);
+    const double theta = fma_rn(c, (double)z2m1, c);
+    const uint32_t kk = (z2m1 + 1u + (1u << 20)) >> 21;
+    const BmPair cs = trigp[kk];
+    const double B = theta - angle[kk];  // exact
+    const double B2 = B * B;
+    const double sb = fma_rn(B * B2, SFB_BMC(kC_S3), B);
+    const double cm1 = B2 * fma_rn(B2, SFB_BMC(kC_C4), SFB_BMC(kC_C2));
+    const double cos_t = fma_rn(cs.x, cm1, fma_rn(-cs.y, sb, cs.x));
+    const double sin_t = fma_rn(cs.y, cm1, fma_rn(cs.x, sb, cs.y));
+    a = (float)(R * cos_t);
+    b = (float)(R * sin_t);
 }
 
 }  // namespace sfb

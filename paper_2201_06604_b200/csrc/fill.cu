@@ -164,53 +164,95 @@ __global__ void __launch_bounds__(256) fill_uniform_fast(int64_t *__restrict__ c
 }
 
 // ---------------------------------------------------------------------------
-// Box-Muller fills (_kernels.py:108-166).  The transform is box_muller_pair()
-// (box_muller.cuh): fp64 throughout, float32 output rounds the fp64 value once.
+// Box-Muller fills (_kernels.py:108-166).  float64 output: box_muller_pair()
+// (box_muller.cuh, fp64 throughout, <= 4 ulp of the reference).  float32
+// output: box_muller_pair_f32() (FAST, the default: ~25 instead of ~45 FP64
+// ops per pair, <= 2^-44 relative) or the float64 transform rounded once
+// (FAST == false, SFB_NORMAL_VARIANT bit 2).
 
-template <typename T>
-__device__ __forceinline__ void put(T *out, int64_t off, double v) {
-    __stcs(out + off, (T)v);
-}
+constexpr int kBmF32Newton = 2;  // rsqrt refinements (the seed is only ~2^-20 accurate)
 
-__device__ __forceinline__ void put4(float *p, double a, double b, double c, double d) {
-    __stcs((float4 *)p, make_float4((float)a, (float)b, (float)c, (float)d));
+__device__ __forceinline__ void put4(float *p, float a, float b, float c, float d) {
+    __stcs((float4 *)p, make_float4(a, b, c, d));
 }
 __device__ __forceinline__ void put4(double *p, double a, double b, double c, double d) {
     __stcs((double2 *)p, make_double2(a, b));
     __stcs((double2 *)p + 1, make_double2(c, d));
 }
-__device__ __forceinline__ void put2(float *p, double a, double b) {
-    __stcs((float2 *)p, make_float2((float)a, (float)b));
+__device__ __forceinline__ void put2(float *p, float a, float b) {
+    __stcs((float2 *)p, make_float2(a, b));
 }
 __device__ __forceinline__ void put2(double *p, double a, double b) {
     __stcs((double2 *)p, make_double2(a, b));
 }
 
-// the 128-bucket log table of box_muller.cuh, staged in shared memory
+// table words of box_muller.cuh (exact form) or the fast float32 tables,
+// staged in shared memory (<= 36.9 KB)
 constexpr int kBmLogWords = 3 * SFB_BM_LOG_N;
 constexpr int kBmTabWords = kBmLogWords + 3 * (SFB_BM_TRIG_N + 1);
+constexpr int kBmSmemBytes = kBmTabWords * 8;
+static_assert(kBmFastLogPairs * 16 + kBmFastTrigPairs * 24 <= kBmSmemBytes, "fast tables fit");
 
-// log table then trig table (box_muller.cuh), staged in shared memory (36.6 KB)
-__device__ __forceinline__ const uint64_t *stage_bm_tables(uint64_t *smem) {
+struct BmView {
+    const uint64_t *logw, *trigw;       // exact form
+    const BmPair *logp, *trigp;         // fast float32 form
+    const double *angle;
+};
+
+template <bool FAST>
+__device__ __forceinline__ BmView stage_bm_tables(unsigned char *raw) {
     static const uint64_t kLogTab[kBmLogWords] = SFB_BM_LOG_TABLE_INIT;
     static const uint64_t kTrigTab[kBmTabWords - kBmLogWords] = SFB_BM_TRIG_TABLE_INIT;
-    for (int t = threadIdx.x; t < kBmLogWords; t += blockDim.x) smem[t] = kLogTab[t];
-    for (int t = threadIdx.x; t < kBmTabWords - kBmLogWords; t += blockDim.x)
-        smem[kBmLogWords + t] = kTrigTab[t];
+    BmView v{};
+    if (FAST) {
+        BmPair *lp = (BmPair *)raw;
+        BmPair *tp = lp + kBmFastLogPairs;
+        double *ang = (double *)(tp + kBmFastTrigPairs);
+        bm_fast_tables(kLogTab, kTrigTab, threadIdx.x, blockDim.x, lp, tp, ang);
+        v.logw = kLogTab;  // global: the rare exact fallback of box_muller_pair_f32
+        v.trigw = kTrigTab;
+        v.logp = lp;
+        v.trigp = tp;
+        v.angle = ang;
+    } else {
+        uint64_t *w = (uint64_t *)raw;
+        for (int t = threadIdx.x; t < kBmLogWords; t += blockDim.x) w[t] = kLogTab[t];
+        for (int t = threadIdx.x; t < kBmTabWords - kBmLogWords; t += blockDim.x)
+            w[kBmLogWords + t] = kTrigTab[t];
+        v.logw = w;
+        v.trigw = w + kBmLogWords;
+    }
     __syncthreads();
-    return smem;
+    return v;
+}
+
+template <bool FAST>
+__device__ __forceinline__ void bm(uint32_t z1, uint32_t z2, const BmView &v, double &a,
+                                   double &b) {
+    box_muller_pair(z1, z2, v.logw, v.trigw, a, b);
+}
+template <bool FAST>
+__device__ __forceinline__ void bm(uint32_t z1, uint32_t z2, const BmView &v, float &a, float &b) {
+    if (FAST) {
+        box_muller_pair_f32<kBmF32Newton>(z1, z2, v.logp, v.trigp, v.angle, v.logw, v.trigw, a,
+                                          b);
+    } else {
+        double da, db;
+        box_muller_pair(z1, z2, v.logw, v.trigw, da, db);
+        a = (float)da;
+        b = (float)db;
+    }
 }
 
 // normal, generic layout: unit = (pair, chunk of pair-iterations)
-template <typename T>
+template <typename T, bool FAST>
 __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__ cur,
                                                            T *__restrict__ out, Geom g,
                                                            int64_t pair_lo, int64_t nloc,
                                                            int64_t chunk, int64_t nunits,
                                                            const __grid_constant__ Pow2Table tab) {
-    __shared__ uint64_t bmtab_s[kBmTabWords];
-    const uint64_t *logtab = stage_bm_tables(bmtab_s);
-    const uint64_t *trigtab = logtab + kBmLogWords;
+    __shared__ __align__(16) unsigned char bm_raw[kBmSmemBytes];
+    const BmView bv = stage_bm_tables<FAST && sizeof(T) == 4>(bm_raw);
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t p = pair_lo + u % nloc;
@@ -229,14 +271,14 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
     skip(tab, sb, (uint64_t)d0);
     int64_t rho = d0 / niter, q = d0 % niter;
     for (int64_t d = d0; d < d1; ++d) {
-        double a, b;
+        T a, b;
         const uint32_t z1 = step_m1(sa);
         const uint32_t z2 = step_m1(sb);
-        box_muller_pair(z1, z2, logtab, trigtab, a, b);
+        bm<FAST>(z1, z2, bv, a, b);
         const int64_t ca = j0 + g.g1 * q;
         const int64_t off = (i + g.g0 * rho) * g.npad + ca;
-        put(out, off, a);
-        if (ca + 1 < g.ncol) put(out, off + 1, b);  // partner discarded past ncol
+        __stcs(out + off, a);
+        if (ca + 1 < g.ncol) __stcs(out + off + 1, b);  // partner discarded past ncol
         if (++q == niter) {
             q = 0;
             ++rho;
@@ -253,15 +295,14 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
 //   PAIRS == 2: g1 % 4 == 0, ncol % 4 == 0, npad % 4 == 0 -> both pairs of a
 //               thread have the same trip count and always-valid partners; one
 //               16-byte store (float32) per trip.
-template <typename T, int PAIRS, int MINB>
+template <typename T, int PAIRS, int MINB, bool FAST>
 __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restrict__ cur,
                                                         T *__restrict__ out, Geom g,
                                                         int64_t i_lo, int64_t nrows_grid,
                                                         int64_t rows_per_chunk, int64_t nunits,
                                                         const __grid_constant__ Pow2Table tab) {
-    __shared__ uint64_t bmtab_s[kBmTabWords];
-    const uint64_t *logtab = stage_bm_tables(bmtab_s);
-    const uint64_t *trigtab = logtab + kBmLogWords;
+    __shared__ __align__(16) unsigned char bm_raw[kBmSmemBytes];
+    const BmView bv = stage_bm_tables<FAST && sizeof(T) == 4>(bm_raw);
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t groups = g.g1 / (2 * PAIRS);
@@ -291,18 +332,18 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
                 for (int k = 0; k < 4; ++k) step3(st[k], z[k][0], z[k][1], z[k][2]);
 #pragma unroll
                 for (int t = 0; t < 3; ++t) {
-                    double a0, b0, a1, b1;
-                    box_muller_pair(z[0][t], z[1][t], logtab, trigtab, a0, b0);
-                    box_muller_pair(z[2][t], z[3][t], logtab, trigtab, a1, b1);
+                    T a0, b0, a1, b1;
+                    bm<FAST>(z[0][t], z[1][t], bv, a0, b0);
+                    bm<FAST>(z[2][t], z[3][t], bv, a1, b1);
                     put4(p + g.g1 * (q + t), a0, b0, a1, b1);
                 }
             }
             for (; q < niter; ++q) {
-                double a0, b0, a1, b1;
+                T a0, b0, a1, b1;
                 const uint32_t z0 = step_m1(st[0]), z1 = step_m1(st[1]);
                 const uint32_t z2 = step_m1(st[2]), z3 = step_m1(st[3]);
-                box_muller_pair(z0, z1, logtab, trigtab, a0, b0);
-                box_muller_pair(z2, z3, logtab, trigtab, a1, b1);
+                bm<FAST>(z0, z1, bv, a0, b0);
+                bm<FAST>(z2, z3, bv, a1, b1);
                 put4(p + g.g1 * q, a0, b0, a1, b1);
             }
         }
@@ -317,25 +358,25 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
                 uint32_t x0, x1, x2, y0, y1, y2;
                 step3(st[0], x0, x1, x2);
                 step3(st[1], y0, y1, y2);
-                double a, b;
-                box_muller_pair(x0, y0, logtab, trigtab, a, b);
+                T a, b;
+                bm<FAST>(x0, y0, bv, a, b);
                 put2(p + g.g1 * q, a, b);
-                box_muller_pair(x1, y1, logtab, trigtab, a, b);
+                bm<FAST>(x1, y1, bv, a, b);
                 put2(p + g.g1 * (q + 1), a, b);
-                box_muller_pair(x2, y2, logtab, trigtab, a, b);
+                bm<FAST>(x2, y2, bv, a, b);
                 put2(p + g.g1 * (q + 2), a, b);
             }
             for (; q < nfull; ++q) {
-                double a, b;
+                T a, b;
                 const uint32_t z1 = step_m1(st[0]), z2 = step_m1(st[1]);
-                box_muller_pair(z1, z2, logtab, trigtab, a, b);
+                bm<FAST>(z1, z2, bv, a, b);
                 put2(p + g.g1 * q, a, b);
             }
             if (nfull < niter) {
-                double a, b;
+                T a, b;
                 const uint32_t z1 = step_m1(st[0]), z2 = step_m1(st[1]);
-                box_muller_pair(z1, z2, logtab, trigtab, a, b);
-                put(p, g.g1 * nfull, a);
+                bm<FAST>(z1, z2, bv, a, b);
+                __stcs(p + g.g1 * nfull, a);
             }
         }
     }
@@ -349,7 +390,13 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
 // host-side launch planning
 
 constexpr int kThreads = 256;
-constexpr int kNormalVariantDefault = 0;
+// measured on B200 (tools/tune.py normal): float32 fast form best at 3
+// CTAs/SM with one pair per thread (variant 10), float64 at 4 CTAs/SM with
+// one pair per thread (variant 3); the spread over all variants is ~8 %
+template <typename T>
+constexpr int normal_variant_default() {
+    return sizeof(T) == 4 ? 10 : 3;
+}
 // enough units to fill 148 SMs several times over (2048 resident threads/SM)
 constexpr int64_t kTargetUnits = 148LL * 2048 * 3;
 constexpr int64_t kMinChunkDraws = 512;
@@ -421,6 +468,40 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
     return launch_check("fill_uniform_generic");
 }
 
+// variant knob (tuning only): bit 0 -> cap registers (4 CTAs/SM), bit 3 ->
+// cap registers (3 CTAs/SM), bit 1 -> one pair per thread even when two fit,
+// bit 2 -> float32 via the exact float64 transform instead of
+// box_muller_pair_f32
+template <typename T, int PAIRS, bool FAST>
+static void launch_normal_fast_minb(int minb, unsigned blocks, cudaStream_t st, int64_t *cur,
+                                    T *out, const Geom &g, int64_t i_lo, int64_t nrows_grid,
+                                    int64_t rpc, int64_t nunits, const Pow2Table &tab) {
+    if (minb >= 4)
+        fill_normal_fast<T, PAIRS, 4, FAST><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                         nrows_grid, rpc, nunits, tab);
+    else if (minb == 3)
+        fill_normal_fast<T, PAIRS, 3, FAST><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                         nrows_grid, rpc, nunits, tab);
+    else
+        fill_normal_fast<T, PAIRS, 1, FAST><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+                                                                         nrows_grid, rpc, nunits, tab);
+}
+
+template <typename T, bool FAST>
+static void launch_normal_fast(bool two, int minb, cudaStream_t st, int64_t *cur, T *out,
+                               const Geom &g, int64_t i_lo, int64_t nrows_grid, int64_t rpc,
+                               int64_t nunits) {
+    Pow2Table tab;
+    pow2_table(&tab);
+    const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
+    if (two)
+        launch_normal_fast_minb<T, 2, FAST>(minb, blocks, st, cur, out, g, i_lo, nrows_grid, rpc,
+                                            nunits, tab);
+    else
+        launch_normal_fast_minb<T, 1, FAST>(minb, blocks, st, cur, out, g, i_lo, nrows_grid, rpc,
+                                            nunits, tab);
+}
+
 template <typename T>
 static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, int64_t item_hi,
                          cudaStream_t st) {
@@ -445,35 +526,27 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
         const int64_t rpc = ceil_div(rows, nchunks);
         nchunks = ceil_div(rows, rpc);
         const int64_t nunits = base * nchunks;
-        const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
-        // variant knob (tuning only): bit 0 -> cap registers (4 CTAs/SM),
-        // bit 1 -> one pair per thread even when two fit
-        const int v = tune_knob("SFB_NORMAL_VARIANT", kNormalVariantDefault);
-        if (two && !(v & 2)) {
-            if (v & 1)
-                fill_normal_fast<T, 2, 4><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
-                                                                       nrows_grid, rpc, nunits, tab);
-            else
-                fill_normal_fast<T, 2, 1><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
-                                                                       nrows_grid, rpc, nunits, tab);
-        } else {
-            const int64_t nunits1 = two ? nunits * 2 : nunits;
-            const unsigned blocks1 = (unsigned)ceil_div(nunits1, kThreads);
-            if (v & 1)
-                fill_normal_fast<T, 1, 4><<<blocks1, kThreads, 0, st>>>(cur, out, g, i_lo,
-                                                                        nrows_grid, rpc, nunits1, tab);
-            else
-                fill_normal_fast<T, 1, 1><<<blocks1, kThreads, 0, st>>>(cur, out, g, i_lo,
-                                                                        nrows_grid, rpc, nunits1, tab);
-        }
+        const int v = tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>());
+        const bool use_two = two && !(v & 2);
+        // one pair per thread where two would fit: twice the units
+        const int64_t nu = (two && !use_two) ? nunits * 2 : nunits;
+        const int minb = (v & 1) ? 4 : (v & 8) ? 3 : 1;
+        if (v & 4)
+            launch_normal_fast<T, false>(use_two, minb, st, cur, out, g, i_lo, nrows_grid, rpc, nu);
+        else
+            launch_normal_fast<T, true>(use_two, minb, st, cur, out, g, i_lo, nrows_grid, rpc, nu);
         return launch_check("fill_normal_fast");
     }
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
     int64_t chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * nloc, kTargetUnits));
     chunk = std::min(chunk, std::max<int64_t>(1, maxdraws));
     const int64_t nunits = nloc * ceil_div(maxdraws, chunk);
-    fill_normal_generic<T><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
-        cur, out, g, pair_lo, nloc, chunk, nunits, tab);
+    if (tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>()) & 4)
+        fill_normal_generic<T, false><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
+            cur, out, g, pair_lo, nloc, chunk, nunits, tab);
+    else
+        fill_normal_generic<T, true><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
+            cur, out, g, pair_lo, nloc, chunk, nunits, tab);
     return launch_check("fill_normal_generic");
 }
 

@@ -6,6 +6,7 @@
 // latency), so the kernel issues DFMA at the pipe's throughput limit.
 #include <cuda_runtime.h>
 
+#include "box_muller.cuh"
 #include "sfb_internal.h"
 
 namespace sfb {
@@ -51,6 +52,12 @@ __global__ void __launch_bounds__(256) write_probe_seg_kernel(double2 *out, int6
     for (; i < b1; i += 256) __stcs(out + i, v);
 }
 
+// rsqrt.approx.f64 seed of box_muller_pair_f32, for the accuracy test
+__global__ void rsqrt_probe_kernel(const double *x, double *y, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = RsqrtSeedHw()(x[i]);
+}
+
 }  // namespace sfb
 
 using namespace sfb;
@@ -75,5 +82,13 @@ extern "C" int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *st
                                                                           0.999999, 1e-7);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "fp64 probe: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+extern "C" int sfb_probe_rsqrt(const double *d_x, double *d_y, int64_t n, void *stream) {
+    if (n <= 0) return SFB_OK;
+    rsqrt_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_x, d_y, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "rsqrt probe: %s", cudaGetErrorString(e));
     return SFB_OK;
 }

@@ -393,6 +393,54 @@ def test_box_muller_port_against_libm():
         assert eq.mean() >= 0.99999, eq.mean()
 
 
+def _host_bm_f32(z1, z2, newton, seed_err):
+    z1 = np.ascontiguousarray(z1, np.int64)
+    z2 = np.ascontiguousarray(z2, np.int64)
+    a = np.empty(len(z1), np.float32)
+    b = np.empty(len(z1), np.float32)
+    _lib.check(_lib.lib().sfb_host_box_muller_f32(
+        _lib.ptr(z1), _lib.ptr(z2), len(z1), newton, seed_err, _lib.ptr(a, _lib._f32p),
+        _lib.ptr(b, _lib._f32p)))
+    return a, b
+
+
+# the device's rsqrt.approx.f64 seed error bound assumed here is asserted on
+# the B200 by tests/test_gpu_parity.py::test_rsqrt_seed_accuracy
+RSQRT_SEED_BOUND = 2.0 ** -19  # measured on B200: 2^-20.06
+
+
+@pytest.mark.parametrize("seed_err", [RSQRT_SEED_BOUND, -RSQRT_SEED_BOUND, 0.0])
+def test_box_muller_f32_form_against_libm(seed_err):
+    """The float32 Box-Muller form (box_muller_pair_f32, the default for
+    float32 output), run on the host with a worst-case modelled rsqrt seed,
+    against float32(reference formula on glibc).  Contract:
+    <= 1 ulp_f32 everywhere (zero crossings included) and identical on
+    >= 99.999 % of cells."""
+    z1, z2 = _bm_draws(2_000_000)
+    a, b = _host_bm_f32(z1, z2, 2, seed_err)  # NEWTON = kBmF32Newton (fill.cu)
+    ra, rb = orc.box_muller(z1, z2)
+    for got, ref in ((a, ra), (b, rb)):
+        r32 = ref.astype(np.float32)
+        d = np.abs(got.astype(np.float64) - r32.astype(np.float64))
+        ulp = np.spacing(np.abs(r32)).astype(np.float64)
+        assert (d <= ulp).all(), (got[d > ulp][:4], r32[d > ulp][:4])
+        assert (got == r32).mean() >= 0.99999, (got == r32).mean()
+
+
+def test_box_muller_f32_form_zero_crossings():
+    """theta on and next to fl(k pi/2): both lanes equal float32(reference)."""
+    near = np.concatenate([k * 2 ** 29 + np.arange(-5000, 5001) for k in (0, 1, 2, 3, 4)])
+    near = near[(near >= 1) & (near <= sf.M1)]
+    rng = np.random.default_rng(5)
+    z1 = rng.integers(1, sf.M1 + 1, len(near))
+    a, b = _host_bm_f32(z1, near, 2, RSQRT_SEED_BOUND)
+    ra, rb = orc.box_muller(z1, near)
+    for got, ref in ((a, ra), (b, rb)):
+        r32 = ref.astype(np.float32)
+        d = np.abs(got.astype(np.float64) - r32.astype(np.float64))
+        assert (d <= np.spacing(np.abs(r32)).astype(np.float64)).all()
+
+
 def _host_fisher(table, n, n_items, reps_override=None, stats=False):
     from scipy.special import gammaln
 
