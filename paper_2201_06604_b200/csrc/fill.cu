@@ -117,8 +117,8 @@ __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict_
 
 // uniform kinds, column-pair fast path (g1 even, npad even, shard = whole pairs)
 // unit = (chunk c, grid row i, pair jp): adjacent lanes = adjacent pairs
-template <int KIND>
-__global__ void __launch_bounds__(256) fill_uniform_fast(int64_t *__restrict__ cur,
+template <int KIND, int MINB, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(int64_t *__restrict__ cur,
                                                          void *__restrict__ out, Geom g,
                                                          int64_t j_lo, int64_t npairs,
                                                          int64_t rows_per_chunk, int64_t nunits,
@@ -448,15 +448,54 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
         const int64_t rows = ceil_div(g.nrow, g.g0);  // max owned rows
         const int64_t base = g.g0 * npairs;
         const int64_t cols = ceil_div(g.ncol, g.g1);
+        // variant knob (tuning only): low 4 bits = unit count in quarters of
+        // kTargetUnits (0 -> 4/4), bits 4-7 = CTAs/SM register cap (0 ->
+        // none), bits 8-11 = dynamic shared memory in 16 KB steps (occupancy
+        // throttle)
+        const int v = tune_knob("SFB_UNIFORM_VARIANT", 0);
+        const int64_t target = kTargetUnits * ((v & 15) ? (v & 15) : 4) / 4;
+        const size_t dsmem = (size_t)((v >> 8) & 15) * 16384;
+        if (dsmem > 48 * 1024) {
+            cudaFuncSetAttribute(fill_uniform_fast<KIND, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+        }
         // chunks of at least max(1, kMinChunkDraws / cols) rows
         const int64_t min_rows = std::max<int64_t>(1, kMinChunkDraws / std::max<int64_t>(1, cols));
-        int64_t nchunks = std::max<int64_t>(1, std::min(ceil_div(kTargetUnits, base),
+        int64_t nchunks = std::max<int64_t>(1, std::min(ceil_div(target, base),
                                                           ceil_div(rows, min_rows)));
         const int64_t rpc = ceil_div(rows, nchunks);
         nchunks = ceil_div(rows, rpc);
         const int64_t nunits = base * nchunks;
-        fill_uniform_fast<KIND><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
-            cur, out, g, j_lo, npairs, rpc, nunits, rate, tab);
+        const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
+        if ((v >> 12) & 3) {  // bits 12-13: 512 / 1024 threads per CTA
+            const int nt = (v >> 12) == 1 ? 512 : 1024;
+            const unsigned b2 = (unsigned)ceil_div(nunits, nt);
+            if (nt == 512)
+                fill_uniform_fast<KIND, 1, 512><<<b2, 512, 0, st>>>(cur, out, g, j_lo, npairs, rpc,
+                                                                   nunits, rate, tab);
+            else
+                fill_uniform_fast<KIND, 1, 1024><<<b2, 1024, 0, st>>>(cur, out, g, j_lo, npairs,
+                                                                     rpc, nunits, rate, tab);
+            return launch_check("fill_uniform_fast");
+        }
+        switch ((v >> 4) & 15) {
+            case 4:
+                fill_uniform_fast<KIND, 4><<<blocks, kThreads, 0, st>>>(cur, out, g, j_lo, npairs,
+                                                                       rpc, nunits, rate, tab);
+                break;
+            case 6:
+                fill_uniform_fast<KIND, 6><<<blocks, kThreads, 0, st>>>(cur, out, g, j_lo, npairs,
+                                                                       rpc, nunits, rate, tab);
+                break;
+            case 8:
+                fill_uniform_fast<KIND, 8><<<blocks, kThreads, 0, st>>>(cur, out, g, j_lo, npairs,
+                                                                       rpc, nunits, rate, tab);
+                break;
+            default:
+                fill_uniform_fast<KIND, 1><<<blocks, kThreads, dsmem, st>>>(cur, out, g, j_lo,
+                                                                           npairs, rpc, nunits,
+                                                                           rate, tab);
+        }
         return launch_check("fill_uniform_fast");
     }
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);

@@ -60,6 +60,23 @@ def fisher_case(table, n, g):
 def main():
     what = sys.argv[1:] or ["normal", "fisher"]
     res = []
+    if "uniform" in what:
+        st = sf.create_streams(sf.set_base_creator(), 1 << 20)[0]
+        cur = st.device_current()
+        out = torch.empty((65536, 65536), dtype=torch.float64, device="cuda")
+
+        def fn():
+            launch_fill("uniform", cur, st.count, out, 65536, 65536, 65536, 1024, 1024)
+
+        for v in (0, 0x1000, 0x2000, 0x1002, 0x2002, 0x1008, 0x2008, 0):
+            os.environ["SFB_UNIFORM_VARIANT"] = str(v)
+            ms = timeit(fn)
+            res.append({"w": "uniform_C5", "variant": hex(v), "ms": ms,
+                        "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
+            print(json.dumps(res[-1]), flush=True)
+        os.environ.pop("SFB_UNIFORM_VARIANT")
+        del out
+        torch.cuda.empty_cache()
     if "normal" in what:
         for dt in (torch.float32, torch.float64):
             fn = normal_case(dt)
