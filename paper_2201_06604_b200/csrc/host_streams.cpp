@@ -16,8 +16,10 @@
 #include <string.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "box_muller.cuh"
@@ -217,67 +219,139 @@ static const char kVersion[] = "v1";                 // core.py:239
 
 int64_t sfb_format_streams_bound(int64_t n) { return 96 + n * 12 * 21; }
 
-static char *put_i64(char *p, int64_t v) {
-    char tmp[24];
-    int k = 0;
-    uint64_t u = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
-    do {
-        tmp[k++] = (char)('0' + u % 10);
-        u /= 10;
-    } while (u);
-    if (v < 0) *p++ = '-';
-    while (k) *p++ = tmp[--k];
-    return p;
+}  // extern "C"
+
+namespace sfb {
+
+// Run f(t, lo, hi) over contiguous ranges of [0, n) on up to one thread per
+// host core (at least `min_per` items per range).  Stream files of 2^20
+// streams are 132 MB: formatting and parsing them are embarrassingly parallel
+// over lines.
+template <typename F>
+static int parallel_ranges(int64_t n, int64_t min_per, F &&f) {
+    const int64_t hw = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), 64));
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hw, n / std::max<int64_t>(1, min_per)));
+    if (nt == 1) {
+        f(0, (int64_t)0, n);
+        return 1;
+    }
+    std::vector<std::thread> pool;
+    for (int64_t t = 1; t < nt; ++t)
+        pool.emplace_back([&f, t, n, nt] { f(t, n * t / nt, n * (t + 1) / nt); });
+    f(0, (int64_t)0, n / nt);
+    for (auto &th : pool) th.join();
+    return (int)nt;
 }
 
-int sfb_format_streams(const int64_t *current, const int64_t *initial, int64_t n,
-                       char *buf, int64_t cap, int64_t *len) {  // core.py:242-250
-    if (cap < sfb_format_streams_bound(n))
-        return fail(SFB_E_INVALID_ARGUMENT, "format buffer too small");
-    char *p = buf;
-    p += snprintf(p, 96, "%s %s count=%lld\n", kMagic, kVersion, (long long)n);
-    for (int64_t k = 0; k < n; ++k) {
+static const char kDigits2[] =
+    "00010203040506070809101112131415161718192021222324252627282930313233343536373839"
+    "40414243444546474849505152535455565758596061626364656667686970717273747576777879"
+    "8081828384858687888990919293949596979899";
+
+static char *put_i64(char *p, int64_t v) {
+    char tmp[24];
+    int k = sizeof tmp;
+    uint64_t u = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+    while (u >= 100) {
+        const unsigned r = (unsigned)(u % 100);
+        u /= 100;
+        tmp[--k] = kDigits2[2 * r + 1];
+        tmp[--k] = kDigits2[2 * r];
+    }
+    if (u >= 10) {
+        tmp[--k] = kDigits2[2 * u + 1];
+        tmp[--k] = kDigits2[2 * u];
+    } else {
+        tmp[--k] = (char)('0' + u);
+    }
+    if (v < 0) *p++ = '-';
+    memcpy(p, tmp + k, sizeof tmp - k);
+    return p + (sizeof tmp - k);
+}
+
+// lines of streams [lo, hi): "c0 .. c5 i0 .. i5\n" (core.py:242-250)
+static char *format_rows(char *p, const int64_t *current, const int64_t *initial, int64_t lo,
+                         int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) {
         for (int c = 0; c < 12; ++c) {
             if (c) *p++ = ' ';
             p = put_i64(p, c < 6 ? current[6 * k + c] : initial[6 * k + c - 6]);
         }
         *p++ = '\n';
     }
+    return p;
+}
+
+// format in parallel: one private buffer per range, in file order
+struct FormattedChunks {
+    std::string header;
+    std::vector<std::vector<char>> parts;
+};
+
+static void format_parallel(const int64_t *current, const int64_t *initial, int64_t n,
+                            FormattedChunks &out) {
+    char hdr[96];
+    snprintf(hdr, sizeof hdr, "%s %s count=%lld\n", kMagic, kVersion, (long long)n);
+    out.header = hdr;
+    const int64_t hw = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), 64));
+    out.parts.assign((size_t)hw, {});
+    parallel_ranges(n, 16384, [&](int64_t t, int64_t lo, int64_t hi) {
+        std::vector<char> &buf = out.parts[(size_t)t];
+        buf.resize((size_t)(hi - lo) * 12 * 21);
+        char *e = format_rows(buf.data(), current, initial, lo, hi);
+        buf.resize((size_t)(e - buf.data()));
+    });
+}
+
+}  // namespace sfb
+
+extern "C" {
+
+int sfb_format_streams(const int64_t *current, const int64_t *initial, int64_t n,
+                       char *buf, int64_t cap, int64_t *len) {  // core.py:242-250
+    if (cap < sfb_format_streams_bound(n))
+        return fail(SFB_E_INVALID_ARGUMENT, "format buffer too small");
+    FormattedChunks fc;
+    format_parallel(current, initial, n, fc);
+    char *p = buf;
+    memcpy(p, fc.header.data(), fc.header.size());
+    p += fc.header.size();
+    for (auto &part : fc.parts) {
+        if (!part.empty()) memcpy(p, part.data(), part.size());
+        p += part.size();
+    }
     *len = p - buf;
+    return SFB_OK;
+}
+
+static int write_all(int fd, const char *p, size_t len, const std::string &name) {
+    while (len) {
+        ssize_t w = write(fd, p, len);
+        if (w < 0) {
+            if (errno == EINTR) continue;
+            return fail(SFB_E_IO, "%s: %s", name.c_str(), strerror(errno));
+        }
+        p += w;
+        len -= (size_t)w;
+    }
     return SFB_OK;
 }
 
 int sfb_save_streams(const char *path, const int64_t *current, const int64_t *initial,
                      int64_t n, int atomic) {  // core.py:242-261
-    const int64_t cap = sfb_format_streams_bound(n);
-    char *buf = (char *)malloc((size_t)cap);
-    if (!buf) return fail(SFB_E_IO, "out of memory formatting %lld streams", (long long)n);
-    int64_t len = 0;
-    int rc = sfb_format_streams(current, initial, n, buf, cap, &len);
-    if (rc) {
-        free(buf);
-        return rc;
-    }
+    FormattedChunks fc;
+    format_parallel(current, initial, n, fc);
     std::string target = path;
     std::string tmp = atomic ? target + ".tmp" : target;
     int fd = open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
-    if (fd < 0) {
-        free(buf);
-        return fail(SFB_E_IO, "%s: %s", tmp.c_str(), strerror(errno));
+    if (fd < 0) return fail(SFB_E_IO, "%s: %s", tmp.c_str(), strerror(errno));
+    int rc = write_all(fd, fc.header.data(), fc.header.size(), tmp);
+    for (size_t t = 0; rc == SFB_OK && t < fc.parts.size(); ++t)
+        rc = write_all(fd, fc.parts[t].data(), fc.parts[t].size(), tmp);
+    if (rc) {
+        close(fd);
+        return rc;
     }
-    int64_t off = 0;
-    while (off < len) {
-        ssize_t w = write(fd, buf + off, (size_t)(len - off));
-        if (w < 0) {
-            if (errno == EINTR) continue;
-            int e = errno;
-            close(fd);
-            free(buf);
-            return fail(SFB_E_IO, "%s: %s", tmp.c_str(), strerror(e));
-        }
-        off += w;
-    }
-    free(buf);
     if (atomic && fsync(fd) != 0) {
         int e = errno;
         close(fd);
@@ -288,6 +362,10 @@ int sfb_save_streams(const char *path, const int64_t *current, const int64_t *in
         return fail(SFB_E_IO, "rename %s: %s", tmp.c_str(), strerror(errno));
     return SFB_OK;
 }
+
+}  // extern "C"
+
+namespace sfb {
 
 // Python str.split() whitespace (ASCII subset)
 static inline bool is_ws(char c) {
@@ -373,6 +451,46 @@ static int parse_header(Cursor &cur, int64_t *count) {  // core.py:271-284
     return SFB_OK;
 }
 
+// the canonical line: 12 unsigned decimal tokens separated by single spaces
+// (what save_streams writes); anything else takes the general tokenizer
+static bool parse_line_fast(const char *b, const char *e, int64_t *vals) {
+    const char *p = b;
+    for (int c = 0; c < 12; ++c) {
+        if (c) {
+            if (p >= e || *p != ' ') return false;
+            ++p;
+        }
+        const char *s = p;
+        uint64_t v = 0;
+        while (p < e && (unsigned)(*p - '0') < 10u) v = v * 10 + (uint64_t)(*p++ - '0');
+        if (p == s || p - s > 18) return false;
+        vals[c] = (int64_t)v;
+    }
+    return p == e;
+}
+
+// one stream line -> 12 values, with the reference's error for a bad line
+// (returns 0 or an error code; msg receives the message)
+static int parse_line(const char *b, const char *e, int64_t k, int64_t *vals, char *msg,
+                      size_t msglen) {
+    if (parse_line_fast(b, e, vals)) return SFB_OK;
+    const char *tb[13], *te[13];
+    if (split(b, e, tb, te, 12) != 12) {
+        snprintf(msg, msglen, "stream %lld: expected 12 integers", (long long)(k + 1));
+        return SFB_E_CORRUPT_STREAM_FILE;
+    }
+    for (int c = 0; c < 12; ++c)
+        if (!parse_int(tb[c], te[c], &vals[c])) {
+            snprintf(msg, msglen, "stream %lld: non-integer entry", (long long)(k + 1));
+            return SFB_E_CORRUPT_STREAM_FILE;
+        }
+    return SFB_OK;
+}
+
+}  // namespace sfb
+
+extern "C" {
+
 int sfb_parse_streams_count(const char *text, int64_t len, int64_t *n) {
     Cursor cur{text, text + len};
     return parse_header(cur, n);
@@ -384,23 +502,88 @@ int sfb_parse_streams(const char *text, int64_t len, int64_t *current, int64_t *
     int64_t count;
     if (int rc = parse_header(cur, &count)) return rc;
     if (count != n) return fail(SFB_E_INVALID_ARGUMENT, "count mismatch");
-    for (int64_t k = 0; k < count; ++k) {
-        const char *b, *e;
-        if (!cur.line(b, e))
-            return fail(SFB_E_CORRUPT_STREAM_FILE, "truncated file: expected %lld streams",
-                        (long long)count);
-        const char *tb[13], *te[13];
-        if (split(b, e, tb, te, 12) != 12)
-            return fail(SFB_E_CORRUPT_STREAM_FILE, "stream %lld: expected 12 integers",
-                        (long long)(k + 1));
-        for (int c = 0; c < 12; ++c) {
-            int64_t v;
-            if (!parse_int(tb[c], te[c], &v))
-                return fail(SFB_E_CORRUPT_STREAM_FILE, "stream %lld: non-integer entry",
-                            (long long)(k + 1));
-            (c < 6 ? current[6 * k + c] : initial[6 * k + c - 6]) = v;
+    // Parallel over byte ranges of the body: pass 1 counts the lines that start
+    // in each range, pass 2 parses lines [0, count) where they start.  The
+    // first error in file order wins, as in the sequential reference loop.
+    const char *body = cur.p, *end = text + len;
+    const int64_t nbytes = end - body;
+    const int64_t hw = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), 64));
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hw, nbytes / (1 << 20)));
+    std::vector<int64_t> starts((size_t)nt + 1, 0), lines((size_t)nt, 0);
+    for (int64_t t = 0; t <= nt; ++t) starts[(size_t)t] = nbytes * t / nt;
+    // a line starts at body[0] or right after a '\n'; it belongs to the range
+    // holding its first byte
+    auto count_starts = [&](int64_t t, int64_t, int64_t) {
+        const int64_t lo = starts[(size_t)t], hi = starts[(size_t)t + 1];
+        int64_t c = (lo == 0 && nbytes > 0) ? 1 : 0;
+        for (const char *q = body + std::max<int64_t>(lo - 1, 0); q < body + hi - 1;) {
+            const char *nl = (const char *)memchr(q, '\n', (size_t)(body + hi - 1 - q));
+            if (!nl) break;
+            if (nl + 1 >= body + lo && nl + 1 < end) ++c;
+            q = nl + 1;
         }
-    }
+        lines[(size_t)t] = c;
+    };
+    if (nt == 1)
+        count_starts(0, 0, 1);
+    else
+        parallel_ranges(nt, 1, [&](int64_t, int64_t lo, int64_t hi) {
+            for (int64_t t = lo; t < hi; ++t) count_starts(t, 0, 0);
+        });
+    std::vector<int64_t> first_line((size_t)nt + 1, 0);
+    for (int64_t t = 0; t < nt; ++t) first_line[(size_t)t + 1] = first_line[(size_t)t] + lines[(size_t)t];
+    const int64_t total_lines = first_line[(size_t)nt];
+    struct Err {
+        int64_t line = INT64_MAX;
+        int code = 0;
+        char msg[160] = {0};
+    };
+    std::vector<Err> errs((size_t)nt);
+    std::vector<const char *> after((size_t)nt, nullptr);  // start of line `count`, if in range t
+    auto parse_range = [&](int64_t t) {
+        const int64_t lo = starts[(size_t)t], hi = starts[(size_t)t + 1];
+        int64_t k = first_line[(size_t)t];
+        // first line start at or after lo
+        const char *q = body + lo;
+        if (lo > 0 && body[lo - 1] != '\n') {
+            const char *nl = (const char *)memchr(q, '\n', (size_t)(end - q));
+            q = nl ? nl + 1 : end;
+        }
+        while (q < body + hi && q < end && k < count) {
+            const char *nl = (const char *)memchr(q, '\n', (size_t)(end - q));
+            const char *e = nl ? nl : end;
+            int64_t vals[12];
+            char msg[160];
+            if (int rc = parse_line(q, e, k, vals, msg, sizeof msg)) {
+                Err &er = errs[(size_t)t];
+                er.line = k;
+                er.code = rc;
+                memcpy(er.msg, msg, sizeof msg);
+                return;
+            }
+            memcpy(current + 6 * k, vals, 6 * sizeof(int64_t));
+            memcpy(initial + 6 * k, vals + 6, 6 * sizeof(int64_t));
+            ++k;
+            q = nl ? nl + 1 : end;
+        }
+        if (k == count && q < body + hi && q < end) after[(size_t)t] = q;
+    };
+    if (nt == 1)
+        parse_range(0);
+    else
+        parallel_ranges(nt, 1, [&](int64_t, int64_t lo, int64_t hi) {
+            for (int64_t t = lo; t < hi; ++t) parse_range(t);
+        });
+    const Err *first = nullptr;
+    for (const Err &er : errs)
+        if (er.code && (!first || er.line < first->line)) first = &er;
+    if (total_lines < count && (!first || first->line >= total_lines))
+        return fail(SFB_E_CORRUPT_STREAM_FILE, "truncated file: expected %lld streams",
+                    (long long)count);
+    if (first) return fail(first->code, "%s", first->msg);
+    cur.p = end;
+    for (const char *q : after)
+        if (q) cur.p = q;
     const char *b, *e;
     if (cur.line(b, e)) {
         for (; b < e; ++b)
