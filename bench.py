@@ -307,6 +307,33 @@ def run_fisher_e2e(torch, sf, steps, table, n, g):
 
 
 # --------------------------------------------------------------- CPU baselines
+def stream_io(api, n=1 << 20):
+    """configs[4] host side: create 2^20 streams, checkpoint them to a stream
+    file (atomic rewrite) and load them back -- the save/restore of the C5
+    checkpoint (core.py:222-305).  `api` is this package or the reference."""
+    import tempfile
+
+    d = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    with tempfile.TemporaryDirectory(dir=d) as tmp:
+        path = os.path.join(tmp, "streams.txt")
+        t0 = time.perf_counter()
+        streams, _ = api.create_streams(api.set_base_creator(), n)
+        t1 = time.perf_counter()
+        save = getattr(api, "save_streams_atomic", None)
+        if save is None:  # the reference keeps it in streamforge.core
+            import importlib
+
+            save = importlib.import_module(api.__name__ + ".core").save_streams_atomic
+        save(streams, path)
+        t2 = time.perf_counter()
+        back = api.load_streams(path)
+        t3 = time.perf_counter()
+        size = os.path.getsize(path)
+    assert np.array_equal(back.current, streams.current)
+    return {"streams": n, "create_s": t1 - t0, "save_s": t2 - t1, "load_s": t3 - t2,
+            "file_bytes": size, "dir": d or "tmp"}
+
+
 def cpu_uniform_sample(orc, rows, threads=0):
     """C5 rows [0, rows) -- every item, rows/g0 owned rows each -- on the oracle."""
     c = C5
@@ -401,6 +428,14 @@ def reference_arm(args, rank, world):
     except Exception as e:  # noqa: BLE001
         line["workloads"] = {"error": str(e)}
     line["numba_reference"] = numba_reference(rows)
+    try:
+        if _import_reference() is None:
+            raise RuntimeError("baseline/_ref not installed")
+        import streamforge as ref_api
+
+        line["workloads"]["stream_io_2p20"] = stream_io(ref_api)
+    except Exception as e:  # noqa: BLE001
+        line["workloads"]["stream_io_2p20"] = {"unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
 
 
@@ -598,6 +633,10 @@ def main():
                                        fp64_ops_per_table=FOPS["T10"],
                                        config=f"configs[3]/C4 shape: T10 sparse 10x10 on grid "
                                               f"(2048,1024), {f10['sim_num']} tables per step")
+    if args.only is None and rank == 0:
+        workloads["stream_io_2p20"] = dict(stream_io(sf), config="configs[4] host side: "
+                                           "create / save_streams_atomic / load_streams of "
+                                           "2^20 streams (C++ creation chain and stream files)")
     e2e = run_uniform_e2e(torch, sf, rank, world, min(args.steps, 3), C5)
     if args.only in (None, "fisher") and world == 1:
         fe = run_fisher_e2e(torch, sf, 3, T4, 10 ** 6, (256, 64))
