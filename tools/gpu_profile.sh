@@ -10,6 +10,11 @@ echo "pytest exit $?" >> gpurun_out/pytest_gpu.txt
 timeout ${BENCH_TIMEOUT:-600} python bench.py ${BENCH_ARGS:---steps 10 --warmup 3} \
     > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench exit $?" >> gpurun_out/bench.err
+if [ -z "$NO_REF" ]; then
+  timeout 900 python bench.py --impl reference --steps 3 --warmup 1 \
+      > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+  echo "reference exit $?" >> gpurun_out/bench_reference.err
+fi
 if [ -z "$NO_NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
       --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 4 --warmup 3 --no-cpu \
