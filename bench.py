@@ -677,7 +677,10 @@ def main():
                      "frac": achieved / peak,
                      "traffic": None if tr_ratio is None else tr_ratio * prim["alg_bytes"],
                      "traffic_source": tr_src,
-                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs, "
+                                  "read+write bytes of a device copy); this kernel only "
+                                  "writes, and a write-only stream can exceed it slightly -- "
+                                  "frac_write against the write-only probe is the tighter bound",
                      "peak_write_measured": wpeak, "frac_write": achieved / wpeak,
                      "kernel": "fill_uniform_fast<0>",
                      "algorithmic_bytes_per_launch": prim["alg_bytes"]},
