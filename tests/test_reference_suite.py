@@ -139,10 +139,9 @@ def test_acceptance_07_table_sampler_distribution(month_table):
         return math.exp(2 * gammaln(6) + 2 * gammaln(6) - gammaln(11)
                         - 2 * gammaln(k + 1) - 2 * gammaln(6 - k))
 
-    # rcont2 is one device launch per table: 2e4 draws instead of 1e5
     counts = np.zeros(6, dtype=np.int64)
     lf10 = log_factorial_table(10)
-    for _ in range(20_000):
+    for _ in range(100_000):
         counts[sf.rcont2([5, 5], [5, 5], state, lf10)[0, 0]] += 1
     expected = np.array([pmf(k) for k in range(6)]) * counts.sum()
     chi2 = ((counts - expected) ** 2 / expected).sum()
