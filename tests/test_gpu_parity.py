@@ -569,3 +569,14 @@ def test_fisher_c4_full_scale_sampled_items(G):
                               plan.reps, int(w) + 1, item_lo=int(w), item_counts=one)
         assert ic[w] == one[0], w
         assert np.array_equal(final[w], ref_st[w]), w
+
+
+def test_chunked_pinned_download_matches_tensor():
+    # MatrixBuffer.download splits large pinned copies over two copy streams
+    import torch
+
+    st = fresh(1 << 14)
+    buf = sf.fill_uniform(st, sf.FillRequest(shape=(4099, 16384), grid=sf.WorkGrid(128, 128)))
+    host = torch.empty((4099, 16384), dtype=torch.float64, pin_memory=True)
+    buf.download(host)
+    assert torch.equal(host, buf.tensor.cpu())
