@@ -563,6 +563,16 @@ def run_probes(torch, _lib):
     return out
 
 
+def ncu_pipes(key):
+    """Pipe utilisation of a compute-bound kernel from the committed ncu capture
+    (profiles/traffic.json, written by tools/summarize_ncu.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)[key]
+    except Exception:
+        return None
+
+
 def ncu_traffic(kernel):
     """dram read+write bytes per algorithmic byte from the committed ncu capture
     (profiles/traffic.json, written by tools/summarize_ncu.py)."""
@@ -652,15 +662,21 @@ def main():
                          "peak_copy": peak, "frac_copy": w["gbs"] / peak,
                          "peak_write": wpeak, "frac_write": w["gbs"] / wpeak,
                          "note": "compute/issue bound: float32 form box_muller_pair_f32, ~91 SASS (30 FP64, 6 XU) per normal pair incl. 2 MRG31k3p steps"}
-    for key, fops in (("fisher_T4_1e6", FOPS["T4"]), ("fisher_T10", FOPS["T10"])):
+    for key, fops, pk in (("fisher_T4_1e6", FOPS["T4"], "pipes_fisher4"),
+                          ("fisher_T10", FOPS["T10"], "pipes_fisher10")):
         if key in workloads:
             w = workloads[key]
             ach = w["value"] * fops
             w["roofline"] = {"bound": "fp64", "achieved": ach / 1e12, "unit": "Tops/s",
                              "peak": probe["fp64_ops_per_s"] / 1e12,
                              "frac": ach / probe["fp64_ops_per_s"],
-                             "note": "source-level FP64 ops per table (SURVEY 8(d)) vs the "
-                                     "measured DFMA issue rate (sfb_probe_fp64)"}
+                             "note": "source-level FP64 ops per table (SURVEY 8(d), a division "
+                                     "counted as 1 op although it issues ~8 FP64 "
+                                     "instructions) vs the measured DFMA issue rate "
+                                     "(sfb_probe_fp64)",
+                             "ncu_pipes": ncu_pipes(pk)}
+    if "rnormGpu_f32_1e9" in workloads:
+        workloads["rnormGpu_f32_1e9"]["roofline"]["ncu_pipes"] = ncu_pipes("pipes_normal")
     achieved = prim["alg_bytes"] / (prim["launch_ms"] / 1e3) / 1e9
     tr_ratio, tr_src = ncu_traffic("fill_uniform_fast")
     line = {

@@ -53,3 +53,40 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def e2e_breakdown(reps=20):
+    """Where the fisher_sim end-to-end time goes (host-authoritative states)."""
+    from paper_2201_06604_b200 import _lib
+
+    grid = sf.WorkGrid(256, 64)
+    st = sf.create_streams(sf.set_base_creator(), grid.size)[0]
+    sf.fisher_sim(T4, 10 ** 6, st, grid=grid)
+    acc = {}
+
+    def tick(k, t0):
+        acc[k] = acc.get(k, 0.0) + time.perf_counter() - t0
+        return time.perf_counter()
+
+    for _ in range(reps):
+        t = time.perf_counter()
+        _ = st.current
+        t = tick("pull states (D2H 786 KB)", t)
+        plan = plan_fisher(np.asarray(T4), 10 ** 6, st, grid)
+        t = tick("plan_fisher (host prep)", t)
+        _lib.require_device()
+        cur = st.device_current()
+        t = tick("push states (H2D 786 KB)", t)
+        cnt = torch.zeros(1, dtype=torch.int64, device=cur.device)
+        t = tick("count alloc+zero", t)
+        launch_fisher(plan, cur, st.count, cnt)
+        t = tick("launch (C ABI)", t)
+        st._mark_device_ahead()
+        int(cnt.item())
+        t = tick("kernel + count.item()", t)
+    for k, v in acc.items():
+        print(f"{k:32s} {1e3 * v / reps:8.3f} ms")
+
+
+if __name__ == "__main__":
+    e2e_breakdown()

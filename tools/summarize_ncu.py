@@ -123,6 +123,27 @@ def main():
                 traffic[kname] = {"dram_bytes": tot, "alg_bytes": abytes,
                                   "source": f"profiles/{tag}/ncu_summary.md "
                                             f"({os.path.basename(rep)}, tools/prof_driver.py {key})"}
+    # pipe utilisation of the compute-bound kernels (bench.py reports it beside
+    # the algorithmic roofline)
+    for rep in args:
+        for key in ("fisher4", "fisher10", "normal"):
+            if f"prof_{key}_" in os.path.basename(rep):
+                raw = ncu_csv(rep, "raw")
+                m = dict(zip(raw[0], raw[2]))
+
+                def f(k):
+                    try:
+                        return float(m[k].replace(",", ""))
+                    except (KeyError, ValueError):
+                        return None
+
+                traffic[f"pipes_{key}"] = {
+                    "fp64_pipe_active_pct": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "issue_slots_busy_pct": f("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+                    "alu_pct": f("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                    "xu_pct": f("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+                    "threads_per_warp_inst": f("smsp__thread_inst_executed_per_inst_executed.ratio"),
+                    "source": f"profiles/{tag}/ncu_summary.md ({os.path.basename(rep)})"}
     if traffic:
         with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
             import json
