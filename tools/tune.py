@@ -90,26 +90,28 @@ def main():
     if "fisher" in what:
         with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
             t10 = np.array(json.load(fh)["T10"])
-        month = np.loadtxt(os.path.join(ROOT, "tests", "golden", "month.csv"), delimiter=",") \
-            if os.path.exists(os.path.join(ROOT, "tests", "golden", "month.csv")) else None
+        month = np.asarray(np.load(os.path.join(ROOT, "tests", "golden", "golden.npz"))["month"])
         only = os.environ.get("TUNE_FISHER_TABLES", "T4,T4x16,T10").split(",")
-        walks = os.environ.get("TUNE_FISHER_WALKS", "1,3").split(",")
         for name, table, n, g in (("T4", T4, 10 ** 6, (256, 64)),
                                   ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
-                                  ("T10", t10, 1 << 23, (2048, 1024))):
+                                  ("T10", t10, 1 << 23, (2048, 1024)),
+                                  ("month", month, 1 << 22, (2048, 1024))):
             if name not in only:
                 continue
             sim, fn, cnt = fisher_case(table, n, g)
-            for walk in walks:
-                for mb in (3, 4):
-                    os.environ["SFB_FISHER_MINB"] = str(mb)
-                    os.environ["SFB_FISHER_WALK"] = walk
-                    ms = timeit(fn, reps=3, warm=1)
-                    fn()
-                    res.append({"w": f"fisher_{name}", "variant": f"walk{walk}_minb{mb}",
-                                "ms": ms, "per_s": sim / (ms / 1e3),
-                                "count_one_launch": int(cnt.item())})
-                    print(json.dumps(res[-1]), flush=True)
+            variants = [("lockstep_minb4", {"SFB_FISHER_PAIR": "0", "SFB_FISHER_MINB": "4"})]
+            for mb in (1, 2, 3):
+                variants.append((f"pair_minb{mb}", {"SFB_FISHER_PAIR": "1",
+                                                    "SFB_FISHER_MINB": str(mb)}))
+            for vname, env in variants:
+                os.environ.update(env)
+                ms = timeit(fn, reps=3, warm=1)
+                fn()
+                res.append({"w": f"fisher_{name}", "variant": vname,
+                            "ms": ms, "per_s": sim / (ms / 1e3),
+                            "count_one_launch": int(cnt.item())})
+                print(json.dumps(res[-1]), flush=True)
+
 
 if __name__ == "__main__":
     main()
