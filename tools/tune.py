@@ -99,10 +99,9 @@ def main():
             if name not in only:
                 continue
             sim, fn, cnt = fisher_case(table, n, g)
-            variants = [("lockstep_minb4", {"SFB_FISHER_PAIR": "0", "SFB_FISHER_MINB": "4"})]
-            for mb in (1, 2, 3):
-                variants.append((f"pair_minb{mb}", {"SFB_FISHER_PAIR": "1",
-                                                    "SFB_FISHER_MINB": str(mb)}))
+            variants = [(f"walk{w}_minb{mb}", {"SFB_FISHER_WALK": str(w),
+                                               "SFB_FISHER_MINB": str(mb)})
+                        for w in (1, 2) for mb in (3, 4)]
             for vname, env in variants:
                 os.environ.update(env)
                 ms = timeit(fn, reps=3, warm=1)
