@@ -200,6 +200,23 @@ def test_normal_layouts_vs_oracle(shape, g, n):
     ref = oa.fill("normal", ref_st, shape, g)
     assert_normal_f64_close(buf.data, ref)
     assert np.array_equal(st.current, ref_st)
+    # float32 form through the same layouts (fast and generic kernels)
+    st = fresh(n)
+    b32 = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=sf.WorkGrid(*g), dtype=np.float32))
+    assert_normal_f32_close(b32.data, ref)
+    assert np.array_equal(st.current, ref_st)
+
+
+@pytest.mark.parametrize("shape,g,n,npad", [((7, 9), (2, 4), 8, 12), ((33, 64), (4, 8), 32, 70),
+                                            ((5, 3), (1, 2), 2, 4)])
+def test_normal_f32_padded_vs_oracle(shape, g, n, npad):
+    st = fresh(n)
+    b32 = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=sf.WorkGrid(*g), npad=npad,
+                                            dtype=np.float32))
+    ref_st = oa.fresh_states(n)
+    ref = oa.fill("normal", ref_st, shape, g, npad=npad)
+    assert_normal_f32_close(b32.data, ref)
+    assert np.array_equal(st.current, ref_st)
 
 
 def test_rsqrt_seed_accuracy():
