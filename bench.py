@@ -698,7 +698,7 @@ def main():
                                   "writes, and a write-only stream can exceed it slightly -- "
                                   "frac_write against the write-only probe is the tighter bound",
                      "peak_write_measured": wpeak, "frac_write": achieved / wpeak,
-                     "kernel": "fill_uniform_fast<0>",
+                     "kernel": "fill_uniform_quad<0> (256-bit stores)",
                      "algorithmic_bytes_per_launch": prim["alg_bytes"]},
         "probes": probe,
         "clocks": prim["clocks"],

@@ -163,6 +163,82 @@ __global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(int64_t *__restric
     }
 }
 
+// uniform kinds, quad fast path (g1 % 4 == 0, npad % 4 == 0, shard = whole
+// quads): one thread drives the four streams of columns j..j+3 and writes them
+// with ONE 32-byte streaming store per owned row step (STG.E.ENL2.256, new on
+// sm_100), so a warp store covers 1 KB contiguous and the LSU issues half the
+// store instructions of the pair path.
+__device__ __forceinline__ void st256(void *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
+                 "l"(d)
+                 : "memory");
+}
+
+template <int KIND>
+__device__ __forceinline__ uint64_t value_bits(uint32_t zm1, double rate) {
+    if (KIND == kInteger) return (uint64_t)zm1 + 1u;
+    return (uint64_t)__double_as_longlong(real_value<KIND>(zm1, rate));
+}
+
+template <int KIND>
+__device__ __forceinline__ void put_quad(void *out, int64_t off, uint32_t z0, uint32_t z1,
+                                         uint32_t z2, uint32_t z3, double rate) {
+    st256((long long *)out + off, value_bits<KIND>(z0, rate), value_bits<KIND>(z1, rate),
+          value_bits<KIND>(z2, rate), value_bits<KIND>(z3, rate));
+}
+
+template <int KIND, int MINB, bool STEP3 = true>
+__global__ void __launch_bounds__(256, MINB) fill_uniform_quad(int64_t *__restrict__ cur,
+                                                         void *__restrict__ out, Geom g,
+                                                         int64_t j_lo, int64_t nquads,
+                                                         int64_t rows_per_chunk, int64_t nunits,
+                                                         double rate, const __grid_constant__ Pow2Table tab) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= nunits) return;
+    const int64_t jq = u % nquads;
+    const int64_t ic = u / nquads;
+    const int64_t i = ic % g.g0, c = ic / g.g0;
+    const int64_t j = j_lo + 4 * jq;
+    const int64_t nr = owned(g.nrow, i, g.g0);
+    const int64_t rho0 = c * rows_per_chunk;
+    if (rho0 >= nr) return;
+    const int64_t rho1 = min(rho0 + rows_per_chunk, nr);
+    int64_t n[4];
+    Mrg s[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        n[k] = owned(g.ncol, j + k, g.g1);  // nonincreasing in k, by at most one
+        s[k] = load_state(cur + 6 * (i + g.g0 * (j + k)));
+        if (rho0) skip(tab, s[k], (uint64_t)(rho0 * n[k]));
+    }
+    for (int64_t rho = rho0; rho < rho1; ++rho) {
+        const int64_t rowoff = (i + g.g0 * rho) * g.npad + j;
+        int64_t q = 0;
+        if (STEP3)
+            for (; q + 3 <= n[3]; q += 3) {  // step3: no shift-register moves
+                uint32_t z[4][3];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) step3(s[k], z[k][0], z[k][1], z[k][2]);
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+                    put_quad<KIND>(out, rowoff + g.g1 * (q + t), z[0][t], z[1][t], z[2][t],
+                                   z[3][t], rate);
+            }
+        for (; q < n[3]; ++q) {
+            const uint32_t z0 = step_m1(s[0]), z1 = step_m1(s[1]);
+            const uint32_t z2 = step_m1(s[2]), z3 = step_m1(s[3]);
+            put_quad<KIND>(out, rowoff + g.g1 * q, z0, z1, z2, z3, rate);
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k)  // ragged last column block
+            if (n[k] > n[3]) put_one<KIND>(out, rowoff + k + g.g1 * n[3], step_m1(s[k]), rate);
+    }
+    if (rho1 == nr) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) store_state(cur + 6 * (i + g.g0 * (j + k)), s[k]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Box-Muller fills (_kernels.py:108-166).  float64 output: box_muller_pair()
 // (box_muller.cuh, fp64 throughout, <= 4 ulp of the reference).  float32
@@ -467,6 +543,41 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
         nchunks = ceil_div(rows, rpc);
         const int64_t nunits = base * nchunks;
         const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
+        const bool quad = !((v >> 14) & 1) && g.g1 % 4 == 0 && g.npad % 4 == 0 &&
+                          (j_lo % 4) == 0 && (npairs % 2) == 0 &&
+                          ((uintptr_t)out & 31) == 0;
+        if (quad) {  // bit 14 set: the pair path instead
+            const int64_t nquads = npairs / 2;
+            const int64_t qbase = g.g0 * nquads;
+            int64_t qchunks = std::max<int64_t>(1, std::min(ceil_div(target, qbase),
+                                                             ceil_div(rows, min_rows)));
+            const int64_t qrpc = ceil_div(rows, qchunks);
+            qchunks = ceil_div(rows, qrpc);
+            const int64_t qunits = qbase * qchunks;
+            const unsigned qb = (unsigned)ceil_div(qunits, kThreads);
+            switch ((v >> 4) & 15) {  // register cap / single-step variants (tuning)
+                case 3:
+                    fill_uniform_quad<KIND, 3><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
+                                                                        qrpc, qunits, rate, tab);
+                    break;
+                case 4:
+                    fill_uniform_quad<KIND, 4><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
+                                                                        qrpc, qunits, rate, tab);
+                    break;
+                case 9:
+                    fill_uniform_quad<KIND, 1, false><<<qb, kThreads, 0, st>>>(
+                        cur, out, g, j_lo, nquads, qrpc, qunits, rate, tab);
+                    break;
+                case 10:
+                    fill_uniform_quad<KIND, 3, false><<<qb, kThreads, 0, st>>>(
+                        cur, out, g, j_lo, nquads, qrpc, qunits, rate, tab);
+                    break;
+                default:
+                    fill_uniform_quad<KIND, 1><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
+                                                                        qrpc, qunits, rate, tab);
+            }
+            return launch_check("fill_uniform_quad");
+        }
         if ((v >> 12) & 3) {  // bits 12-13: 512 / 1024 threads per CTA
             const int nt = (v >> 12) == 1 ? 512 : 1024;
             const unsigned b2 = (unsigned)ceil_div(nunits, nt);
