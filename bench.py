@@ -678,7 +678,7 @@ def main():
     if "rnormGpu_f32_1e9" in workloads:
         workloads["rnormGpu_f32_1e9"]["roofline"]["ncu_pipes"] = ncu_pipes("pipes_normal")
     achieved = prim["alg_bytes"] / (prim["launch_ms"] / 1e3) / 1e9
-    tr_ratio, tr_src = ncu_traffic("fill_uniform_fast")
+    tr_ratio, tr_src = ncu_traffic("fill_uniform")
     line = {
         "metric": METRIC, "value": prim["value"], "unit": "uniforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": prim["ms_per_step"],

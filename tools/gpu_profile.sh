@@ -21,7 +21,7 @@ if [ -z "$NO_NCU" ]; then
       > gpurun_out/ncu_bench_stdout.txt 2>&1
   for K in ${KERNELS:-uniform normal fisher4 fisher10}; do
     case $K in
-      uniform) RX="fill_uniform_fast";;
+      uniform) RX="fill_uniform_";;
       normal) RX="fill_normal_fast";;
       fisher4|fisher10) RX="fisher_kernel";;
     esac

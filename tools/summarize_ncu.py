@@ -108,7 +108,7 @@ def main():
         for rep in args:
             fh.write(summarize(rep) + "\n")
     # traffic per algorithmic byte for the HBM-bound kernels (bench.py reads it)
-    alg = {"uniform": ("fill_uniform_fast", 4096 * 65536 * 8 + (1 << 20) * 96),
+    alg = {"uniform": ("fill_uniform", 4096 * 65536 * 8 + (1 << 20) * 96),
            "normal": ("fill_normal_fast", (31250 // 8) * 32000 * 4 + (1 << 18) * 96)}
     traffic = {}
     for rep in args:
