@@ -47,9 +47,14 @@ __device__ __forceinline__ int64_t owned(int64_t n, int64_t idx, int64_t g) {
     return idx < n ? (n - idx + g - 1) / g : 0;
 }
 
-// u = z * NORM (_kernels.py:70) from zm1 = z - 1: fma(zm1, 2^-31, 2^-31) is exact
+// u = z * NORM (_kernels.py:70) from zm1 = z - 1, without an int->double
+// conversion (I2F.F64 runs on the narrow XU pipe): the register pair
+// (lo = zm1, hi = 0x43300000) is the double M = 2^52 + zm1, and
+// fma(M, 2^-31, 2^-31 - 2^21) = zm1 2^-31 + 2^-31 exactly (M 2^-31 is an
+// exact power-of-two scaling and the sum is representable), i.e. one DFMA.
 __device__ __forceinline__ double u01(uint32_t zm1) {
-    return __fma_rn((double)zm1, kNorm, kNorm);
+    const double m = __hiloint2double(0x43300000, (int)zm1);
+    return __fma_rn(m, kNorm, kNorm - 0x1p21);
 }
 
 template <int KIND>
