@@ -198,32 +198,49 @@ def run_uniform(torch, sf, rank, world, steps, warmup, cfg, kind="uniform"):
 
 
 def run_uniform_e2e(torch, sf, rank, world, steps, cfg):
-    """Public API with host buffers: states uploaded from the host StreamSet,
-    fill_uniform(...), matrix downloaded into a pinned host array, each step."""
-    if world > 1:
-        return None  # the e2e leg is reported at N=1 (host RAM per rank)
+    """Public API with host buffers, every step: host states uploaded, the fill,
+    the result downloaded into pinned host memory.  N = 1: fill_uniform and the
+    whole matrix.  N > 1: run_grid_sharded (the multi-GPU API: each rank fills
+    its stream block, states all-gathered) and each rank downloads its own
+    cells (MatrixBuffer.download_shard) -- the output stays sharded."""
     g = sf.WorkGrid(cfg["g0"], cfg["g1"])
     st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
-    req = sf.FillRequest(shape=(cfg["nrow"], cfg["ncol"]), grid=g)
-    host = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=torch.float64, pin_memory=True)
+    values = cfg["nrow"] * cfg["ncol"]
+    if world == 1:
+        req = sf.FillRequest(shape=(cfg["nrow"], cfg["ncol"]), grid=g)
+        host = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=torch.float64, pin_memory=True)
+
+        def step():
+            _ = st.current  # host-authoritative states: the next call uploads them
+            buf = sf.fill_uniform(st, req)
+            buf.download(host)
+    else:
+        from paper_2201_06604_b200.sharding import fill_shard, run_grid_sharded
+
+        lo, hi = fill_shard("uniform", cfg["g0"], cfg["g1"], rank, world)
+        j_lo, j_hi = lo // cfg["g0"], hi // cfg["g0"]
+        host = torch.empty(cfg["nrow"] * (cfg["ncol"] // cfg["g1"]) * (j_hi - j_lo),
+                           dtype=torch.float64, pin_memory=True)
+
+        def step():
+            _ = st.current
+            buf = run_grid_sharded(st, g, cfg["nrow"], cfg["ncol"], "uniform")
+            buf.download_shard(cfg["g1"], j_lo, j_hi, host)
     tm = Timer(torch)
-    buf = sf.fill_uniform(st, req)  # warm-up
-    buf.download(host)
-    del buf
+    step()  # warm-up
     torch.cuda.synchronize()
+    barrier(torch, world)
     t0 = time.perf_counter()
     tm.start()
     for _ in range(steps):
-        _ = st.current  # host-authoritative states: the next call uploads them
-        buf = sf.fill_uniform(st, req)
-        buf.download(host)
-        del buf
+        step()
     ms = tm.stop()
+    barrier(torch, world)
+    ms = max_over_ranks(torch, world, ms)
     wall = time.perf_counter() - t0
-    values = cfg["nrow"] * cfg["ncol"]
     return dict(value=values * steps / (ms / 1e3), unit="uniforms/s",
-                h2d_bytes_per_step=cfg["n_streams"] * 48,
-                d2h_bytes_per_step=values * 8 + cfg["n_streams"] * 48 * 0,
+                h2d_bytes_per_step=cfg["n_streams"] * 48 * world,
+                d2h_bytes_per_step=values * 8,
                 wall_s=wall, steps=steps)
 
 

@@ -105,6 +105,13 @@ int sfb_fill_integer(int64_t *d_cur, int64_t n_streams, int64_t *d_out,
  * float32 extension rounds the fp64 result once).  Shard range [item_lo,
  * item_hi) is in stream ordinals and must be pair aligned.  g1 must be even
  * (SFB_E_INVALID_GRID, grid.py:37-40). */
+/* multi-GPU e2e helper (no reference counterpart: the reference has one host):
+ * copy the cells of grid columns [j_lo, j_hi) -- columns c = j + g1 q of a
+ * rank's uniform-kind shard -- from the (nrow, npad) device matrix into a
+ * packed host array, row-major over (row, q, j).  Stream-ordered. */
+int sfb_download_shard(void *dst_host, const void *src_dev, int64_t nrow, int64_t ncol,
+                       int64_t npad, int64_t g1, int64_t j_lo, int64_t j_hi, int64_t elsize,
+                       void *stream);
 int sfb_fill_normal(int64_t *d_cur, int64_t n_streams, void *d_out, int out_dtype,
                     int64_t nrow, int64_t ncol, int64_t npad, int64_t g0,
                     int64_t g1, int64_t item_lo, int64_t item_hi, int zero_pad,

@@ -63,6 +63,7 @@ _SIGS = {
     "sfb_rcont2_table": ([_i64p, _int, _i64p, _int, _f64p, _i64, _vp, _vp, _vp], _int),
     "sfb_probe_fp64": ([_vp, _i64, _int, _vp], _int),
     "sfb_probe_rsqrt": ([_vp, _vp, _i64, _vp], _int),
+    "sfb_download_shard": ([_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp], _int),
     "sfb_probe_write": ([_vp, _i64, _int, _vp], _int),
     "sfb_host_step_u32": ([_i64p, _i64, _i64, _i64p], _int),
     "sfb_host_exp": ([ctypes.c_double], ctypes.c_double),

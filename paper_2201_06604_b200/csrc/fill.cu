@@ -769,4 +769,45 @@ int sfb_fill_normal(int64_t *d_cur, int64_t n_streams, void *d_out, int out_dtyp
     return launch_normal<float>(d_cur, (float *)d_out, g, item_lo, item_hi, st);
 }
 
+int sfb_download_shard(void *dst_host, const void *src_dev, int64_t nrow, int64_t ncol,
+                       int64_t npad, int64_t g1, int64_t j_lo, int64_t j_hi, int64_t elsize,
+                       void *stream) {
+    if (nrow < 1 || ncol < 1 || npad < ncol || g1 < 1 || elsize < 1)
+        return fail(SFB_E_INVALID_ARGUMENT, "bad shard geometry");
+    if (j_lo < 0 || j_hi > g1 || j_lo > j_hi)
+        return fail(SFB_E_INVALID_ARGUMENT, "column range [%lld, %lld) outside [0, %lld)",
+                    (long long)j_lo, (long long)j_hi, (long long)g1);
+    const int64_t w = j_hi - j_lo;
+    if (w == 0) return SFB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t es = (size_t)elsize;
+    cudaError_t e = cudaSuccess;
+    if (npad == ncol && ncol % g1 == 0) {
+        // every run is w elements at pitch g1 across the whole matrix: one 2-D copy
+        const int64_t runs = nrow * (ncol / g1);
+        e = cudaMemcpy2DAsync(dst_host, w * es, (const char *)src_dev + j_lo * es, g1 * es,
+                              w * es, (size_t)runs, cudaMemcpyDeviceToHost, st);
+    } else {
+        // row by row: runs c = j + g1 q, the last one possibly ragged
+        char *dst = (char *)dst_host;
+        for (int64_t r = 0; r < nrow && e == cudaSuccess; ++r) {
+            const char *row = (const char *)src_dev + (size_t)(r * npad) * es;
+            const int64_t full = ncol / g1, rem = ncol - full * g1;
+            if (full) {
+                e = cudaMemcpy2DAsync(dst, w * es, row + j_lo * es, g1 * es, w * es, (size_t)full,
+                                      cudaMemcpyDeviceToHost, st);
+                dst += (size_t)(full * w) * es;
+            }
+            const int64_t tail = std::min(j_hi, rem) - j_lo;
+            if (e == cudaSuccess && tail > 0) {
+                e = cudaMemcpyAsync(dst, row + (full * g1 + j_lo) * es, (size_t)tail * es,
+                                    cudaMemcpyDeviceToHost, st);
+                dst += (size_t)tail * es;
+            }
+        }
+    }
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "shard download: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
 }  // extern "C"

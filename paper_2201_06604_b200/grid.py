@@ -137,6 +137,26 @@ class MatrixBuffer:
             s.synchronize()
         return out
 
+    def download_shard(self, g1: int, j_lo: int, j_hi: int, out=None):
+        """Copy the cells of grid columns [j_lo, j_hi) (a rank's uniform-kind
+        shard: columns c = j + g1 q) into a packed host array, row-major over
+        (row, q, j) -- what one rank of a multi-GPU fill keeps on its host.
+        `out` (numpy or pinned torch CPU tensor) must hold exactly those cells."""
+        import torch
+
+        cells = sum(len(range(j, self.ncol, g1)) for j in range(j_lo, j_hi)) * self.nrow
+        if out is None:
+            out = torch.empty(cells, dtype=self.tensor.dtype, pin_memory=True)
+        dst = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+        if dst.numel() != cells or not dst.is_contiguous():
+            raise InvalidArgumentError(f"shard download needs a contiguous buffer of {cells} cells")
+        st = torch.cuda.current_stream(self.tensor.device)
+        _lib.check(_lib.lib().sfb_download_shard(
+            dst.data_ptr(), self.tensor.data_ptr(), self.nrow, self.ncol, self.npad, g1, j_lo,
+            j_hi, self.tensor.element_size(), st.cuda_stream))
+        st.synchronize()
+        return out
+
     @property
     def device_values(self):
         """The logical nrow x ncol submatrix as a CUDA tensor view (no copy)."""

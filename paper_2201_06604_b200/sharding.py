@@ -41,7 +41,8 @@ def fill_shard(kind: str, g0: int, g1: int, rank: int, world: int):
     """Stream-ordinal block of `rank` for a fill of this kind on a (g0, g1) grid."""
     if kind == "normal":
         return shard_range(g0 * g1, rank, world, align=g1)  # whole grid rows
-    align = 2 * g0 if g1 % 2 == 0 else g0  # whole column pairs when possible
+    # whole column quads (the 256-bit store kernel) or pairs when possible
+    align = 4 * g0 if g1 % 4 == 0 else 2 * g0 if g1 % 2 == 0 else g0
     return shard_range(g0 * g1, rank, world, align=align)
 
 

@@ -597,3 +597,19 @@ def test_chunked_pinned_download_matches_tensor():
     host = torch.empty((4099, 16384), dtype=torch.float64, pin_memory=True)
     buf.download(host)
     assert torch.equal(host, buf.tensor.cpu())
+
+
+@pytest.mark.parametrize("shape,g1,jr", [((64, 4096), 1024, (128, 256)), ((33, 1000), 64, (4, 12)),
+                                         ((5, 70), 32, (0, 32))])
+def test_download_shard_matches_column_selection(shape, g1, jr):
+    # MatrixBuffer.download_shard: a rank's grid columns, packed (row, q, j)
+    import torch
+
+    g0 = 4
+    st = fresh(g0 * g1)
+    buf = sf.fill_uniform(st, sf.FillRequest(shape=shape, grid=sf.WorkGrid(g0, g1)))
+    got = buf.download_shard(g1, *jr).numpy()
+    full = buf.values
+    want = np.concatenate([full[r, [c for c in range(shape[1]) if jr[0] <= c % g1 < jr[1]]]
+                           for r in range(shape[0])])
+    assert np.array_equal(got, want)
