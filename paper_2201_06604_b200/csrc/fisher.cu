@@ -62,6 +62,10 @@ struct FisherArgs {
     int nr, nc, ntot, lf_len;
     MemoSet memo;  // memoised first-row / first-column walks
     int use_memo;
+    // small memo sets are staged into shared memory: the device block holding
+    // row | col | cfg | acc | k (16-byte aligned, memo_bytes long)
+    const unsigned char *memo_blob;
+    int memo_bytes;  // > 0: stage into shared memory
 };
 
 struct LfGlobal {
@@ -89,6 +93,22 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         for (int t = threadIdx.x; t < a.lf_len; t += blockDim.x) lfs[t] = a.lf[t];
     __syncthreads();
 
+    // small memo sets: one cooperative copy into shared memory, pointers rebased
+    MemoSet memo = a.memo;
+    if (a.memo_bytes > 0) {
+        uint4 *dst = (uint4 *)(((uintptr_t)(jwork + (a.nc > 1 ? a.nc - 1 : 1) * blockDim.x) + 15) &
+                               ~(uintptr_t)15);
+        const uint4 *src = (const uint4 *)a.memo_blob;
+        for (int t = threadIdx.x; t < (a.memo_bytes + 15) / 16; t += blockDim.x) dst[t] = src[t];
+        const unsigned char *base = (const unsigned char *)dst;
+        auto rebase = [&](const void *p) { return base + ((const unsigned char *)p - a.memo_blob); };
+        memo.row = (const MemoCellDesc *)rebase(a.memo.row);
+        memo.col = (const MemoCellDesc *)rebase(a.memo.col);
+        memo.cfg = (const MemoConfig *)rebase(a.memo.cfg);
+        memo.acc = (const double *)rebase(a.memo.acc);
+        memo.k = (const int32_t *)rebase(a.memo.k);
+        __syncthreads();
+    }
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int hits = 0;
     if (u < a.nunits) {
@@ -101,7 +121,6 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
             Mrg s = load_state(a.cur + 6 * w);
             if (c) apply(jumps.j[c], s);
             int *jw = jwork + threadIdx.x;
-            const MemoSet memo = a.memo;
             const MemoSet *mp = a.use_memo ? &memo : nullptr;
             for (int64_t rep = rep0; rep < rep1; ++rep) {
                 double stat;
@@ -206,6 +225,8 @@ struct StagedInputs {
     int32_t *rowm = nullptr, *colm = nullptr;
     double *lf = nullptr;
     MemoSet memo{};
+    const unsigned char *memo_blob = nullptr;
+    size_t memo_bytes = 0;
     // record the consumer kernel (call after the launch)
     void done(cudaStream_t st) {
         if (cache->last_use == nullptr)
@@ -246,9 +267,9 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
     if (c.key != host || c.memo_version != memo_version) {
         cudaError_t e = cudaSuccess;
         if (c.pending) e = cudaEventSynchronize(c.last_use);  // previous readers done
-        if (e == cudaSuccess && bytes > c.dev_cap) {
+        if (e == cudaSuccess && bytes + 64 > c.dev_cap) {
             if (c.dev) cudaFree(c.dev);
-            c.dev_cap = std::max(bytes, (size_t)1 << 20);
+            c.dev_cap = std::max(bytes + 64, (size_t)1 << 20);  // +64: 16-byte block copies
             e = cudaMalloc((void **)&c.dev, c.dev_cap);
         }
         if (e == cudaSuccess && bytes > c.pin_cap) {
@@ -284,11 +305,14 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
     out.rowm = (int32_t *)c.dev;
     out.colm = out.rowm + nr;
     out.lf = (double *)(c.dev + lf_off);
-    if (hm)
+    if (hm) {
         out.memo = MemoSet{(const MemoCellDesc *)(c.dev + row_off),
                            (const MemoCellDesc *)(c.dev + col_off),
                            (const MemoConfig *)(c.dev + cfg_off), (const double *)(c.dev + acc_off),
                            (const int32_t *)(c.dev + k_off)};
+        out.memo_blob = c.dev + row_off;
+        out.memo_bytes = bytes - row_off;
+    }
     return SFB_OK;
 }
 
@@ -434,12 +458,21 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     a.lf_len = (int)lf_len;
     a.memo = in.memo;
     a.use_memo = use_memo ? 1 : 0;
+    a.memo_blob = in.memo_blob;
+    a.memo_bytes = 0;
 
     const size_t head = 2048 + (size_t)(nr + nc) * 4 + 16;
     const size_t jw = (size_t)std::max(nc - 1, 1) * kFisherThreads * 4;
     const size_t lf_bytes = (size_t)lf_len * 8;
     const bool lf_smem = head + lf_bytes + jw <= 110 * 1024;
-    const size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
+    size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
+    // memo tables small enough to share the CTA's budget (T4: 22 KB) live in
+    // shared memory: their binary searches then cost ~30 instead of ~500 cycles
+    if (use_memo && in.memo_bytes > 0 &&
+        smem + 16 + in.memo_bytes <= (size_t)tune_knob("SFB_FISHER_MEMO_SMEM_KB", 48) * 1024) {
+        a.memo_bytes = (int)in.memo_bytes;
+        smem += 16 + in.memo_bytes;
+    }
     const unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
     if (smem > (size_t)kMaxFisherSmem)
         return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
