@@ -664,6 +664,16 @@ def main():
         workloads["stream_io_2p20"] = dict(stream_io(sf), config="configs[4] host side: "
                                            "create / save_streams_atomic / load_streams of "
                                            "2^20 streams (C++ creation chain and stream files)")
+    if args.only in (None, "fisher") and (world >= 8 or os.environ.get("SFB_BENCH_C4") == "1"):
+        # configs[3]/C4 in full: T10, 1e10 tables on grid (2048,1024), 2^21
+        # streams, sharded by items + one all-reduce (~2 s per step on 8 B200)
+        t10 = np.array(_t10())
+        c4 = run_fisher(torch, sf, rank, world, 1, 1, t10, 10 ** 10, (2048, 1024), scratch)
+        workloads["fisher_C4_1e10"] = dict(value=c4["value"], unit="tables/s",
+                                           ms_per_step=c4["ms_per_step"], sim_num=c4["sim_num"],
+                                           counts=c4["counts_last"],
+                                           config="configs[3]/C4: T10, 1e10 -> 10001317888 "
+                                                  "tables on grid (2048,1024), 2^21 streams")
     e2e = run_uniform_e2e(torch, sf, rank, world, min(args.steps, 3), C5)
     if args.only in (None, "fisher") and world == 1:
         fe = run_fisher_e2e(torch, sf, 3, T4, 10 ** 6, (256, 64))
