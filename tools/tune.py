@@ -99,9 +99,9 @@ def main():
             if name not in only:
                 continue
             sim, fn, cnt = fisher_case(table, n, g)
-            variants = [(f"memo_smem{kb}_minb{mb}", {"SFB_FISHER_MEMO_SMEM_KB": str(kb),
-                                                     "SFB_FISHER_MINB": str(mb)})
-                        for kb in (0, 48) for mb in (3, 4)]
+            variants = [(f"walk{w}_minb{mb}", {"SFB_FISHER_WALK": str(w),
+                                               "SFB_FISHER_MINB": str(mb)})
+                        for w in (1, 3) for mb in (3, 4)]
             for vname, env in variants:
                 os.environ.update(env)
                 ms = timeit(fn, reps=3, warm=1)
