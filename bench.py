@@ -167,7 +167,7 @@ def run_uniform(torch, sf, rank, world, steps, warmup, cfg, kind="uniform"):
 
     g0, g1 = cfg["g0"], cfg["g1"]
     st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
-    lo, hi = shard(g0 * g1, rank, world, align=2 * g0)
+    lo, hi = shard(g0 * g1, rank, world, align=4 * g0 if g1 % 4 == 0 else 2 * g0)
     cur = st.device_current()
     dt = torch.int64 if kind == "uniform-integer" else torch.float64
     out = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=dt, device="cuda")
