@@ -39,6 +39,7 @@ extern "C" {
 #define SFB_E_INVALID_SEED (-6)          /* errors.py:8 InvalidSeedError */
 #define SFB_E_CORRUPT_STREAM_FILE (-7)   /* errors.py:16 CorruptStreamFileError */
 #define SFB_E_IO (-8)                    /* OSError from open()/write() */
+#define SFB_E_INVALID_PARAMS (-9)        /* errors.py:36 InvalidParamsError (GRF) */
 #define SFB_E_CUDA (-100)                /* CUDA runtime / launch failure */
 
 /* output element types */
@@ -105,6 +106,24 @@ int sfb_fill_integer(int64_t *d_cur, int64_t n_streams, int64_t *d_out,
  * float32 extension rounds the fp64 result once).  Shard range [item_lo,
  * item_hi) is in stream ordinals and must be pair aligned.  g1 must be even
  * (SFB_E_INVALID_GRID, grid.py:37-40). */
+/* ---- Gaussian random fields (grf.py:116-187) -------- */
+/* grf.py:116-124 bessel_k: K_nu(x) elementwise on device arrays (nu > 0, x > 0
+ * validated by the caller); ~1e-13 relative to scipy.special.kv */
+int sfb_bessel_k(double nu, const double *d_x, int64_t n, double *d_out, void *stream);
+/* grf.py:138-159 matern_correlation at distances d (1 at d == 0) */
+int sfb_matern_correlation(double kappa, double range, const double *d_dist, int64_t n,
+                           double *d_out, void *stream);
+/* grf.py:170-187 matern_cov: nb blocks of n x n into d_out (nb*n, n).
+ * params: nb rows of (shape, range, variance, aniso_ratio, aniso_angle), host.
+ * nx*ny == n: a regular GridSpec (cells row-major over (y, x), spacing `cell`)
+ * -> one correlation per distinct index offset; otherwise d_coords (n, 2).
+ * d_scratch: sfb_matern_scratch_bytes(nb, nx, ny) bytes of device memory. */
+int sfb_matern_cov(const double *params, int nb, const double *d_coords, int64_t n, int nx,
+                   int ny, double cell, double *d_scratch, double *d_out, void *stream);
+int64_t sfb_matern_scratch_bytes(int nb, int nx, int ny);
+/* CPU test hook: the same K_nu on the host */
+double sfb_host_bessel_k(double nu, double x);
+
 /* multi-GPU e2e helper (no reference counterpart: the reference has one host):
  * copy the cells of grid columns [j_lo, j_hi) -- columns c = j + g1 q of a
  * rank's uniform-kind shard -- from the (nrow, npad) device matrix into a

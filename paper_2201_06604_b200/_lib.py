@@ -26,6 +26,7 @@ _ERRORS = {
     -6: errors.InvalidSeedError,
     -7: errors.CorruptStreamFileError,
     -8: OSError,
+    -9: errors.InvalidParamsError,
     -100: errors.DeviceError,
 }
 
@@ -63,6 +64,11 @@ _SIGS = {
     "sfb_rcont2_table": ([_i64p, _int, _i64p, _int, _f64p, _i64, _vp, _vp, _vp], _int),
     "sfb_probe_fp64": ([_vp, _i64, _int, _vp], _int),
     "sfb_probe_rsqrt": ([_vp, _vp, _i64, _vp], _int),
+    "sfb_bessel_k": ([ctypes.c_double, _vp, _i64, _vp, _vp], _int),
+    "sfb_matern_correlation": ([ctypes.c_double, ctypes.c_double, _vp, _i64, _vp, _vp], _int),
+    "sfb_matern_cov": ([_f64p, _int, _vp, _i64, _int, _int, ctypes.c_double, _vp, _vp, _vp], _int),
+    "sfb_matern_scratch_bytes": ([_int, _int, _int], _i64),
+    "sfb_host_bessel_k": ([ctypes.c_double, ctypes.c_double], ctypes.c_double),
     "sfb_download_shard": ([_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp], _int),
     "sfb_probe_write": ([_vp, _i64, _int, _vp], _int),
     "sfb_host_step_u32": ([_i64p, _i64, _i64, _i64p], _int),
