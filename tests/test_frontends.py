@@ -310,3 +310,84 @@ class TestServiceCompute:
         assert body["p_value"] == expect.p_value
         assert body["statistics"] == expect.statistics.tolist()
         assert round(body["threshold"]) == -47955
+
+
+# ----------------------------------------------------------------- GRF front-ends
+def params_file(tmp_path, header="shape,range,variance,anisoRatio,anisoAngleRadians",
+                rows=("1.0,2.0,1.0,1.0,0.0", "0.5,3.0,2.0,1.0,0.0")):
+    p = tmp_path / "params.csv"
+    p.write_text(header + "\n" + "\n".join(rows) + "\n")
+    return str(p)
+
+
+def test_grf_missing_parameter_column_named(runner, tmp_path):
+    """reference tests/test_cli.py:238-253."""
+    path = tmp_path / "s.txt"
+    stream_file(path, 16)
+    res = runner.invoke(main, ["grf", "--params", params_file(
+        tmp_path, header="shape,range,variance,anisoRatio", rows=("1,2,1,1",)),
+        "--ncell-x", "2", "--ncell-y", "2", "--cell-size", "1.0", "--grid", "4x4",
+        "--streams", str(path), "--out-dir", str(tmp_path / "o")])
+    assert res.exit_code == 2
+    assert "anisoAngleRadians" in res.output
+
+
+@pytest.mark.gpu
+class TestGrfFrontends:
+    def test_cli_writes_fields_and_manifest(self, runner, tmp_path):
+        import json
+
+        path = tmp_path / "s.txt"
+        stream_file(path, 16)
+        out_dir = tmp_path / "fields"
+        res = runner.invoke(main, ["grf", "--params", params_file(tmp_path), "--ncell-x", "5",
+                                   "--ncell-y", "4", "--cell-size", "1.0", "--realizations", "2",
+                                   "--grid", "4x4", "--streams", str(path), "--out-dir",
+                                   str(out_dir)])
+        assert res.exit_code == 0, res.output
+        manifest = json.loads((out_dir / "manifest.json").read_text())
+        assert len(manifest) == 4 and manifest[0]["params"]["shape"] == 1.0
+        direct = sf.simulate_grf([sf.MaternParams(1.0, 2.0, 1.0), sf.MaternParams(0.5, 3.0, 2.0)],
+                                 sf.GridSpec(5, 4, 1.0), 2,
+                                 sf.create_streams(sf.set_base_creator(), 16)[0],
+                                 sf.WorkGrid(4, 4))
+        for e in manifest:
+            f = np.loadtxt(str(out_dir / e["file"]), delimiter=",")
+            assert f.shape == (4, 5)
+            assert np.array_equal(f, direct[e["parameter_row"] - 1, e["realization"] - 1])
+
+    def test_cli_bin_format_round_trips(self, runner, tmp_path):
+        import struct
+
+        outs = {}
+        for fmt in ("csv", "bin"):
+            path = tmp_path / f"s_{fmt}.txt"
+            stream_file(path, 16)
+            res = runner.invoke(main, ["grf", "--params", params_file(tmp_path), "--ncell-x",
+                                       "3", "--ncell-y", "3", "--cell-size", "1.0", "--grid",
+                                       "4x4", "--streams", str(path), "--out-dir",
+                                       str(tmp_path / fmt), "--format", fmt])
+            assert res.exit_code == 0, res.output
+            outs[fmt] = tmp_path / fmt
+        raw = (outs["bin"] / "field_p1_r1.bin").read_bytes()
+        assert struct.unpack("<IIQ", raw[:16]) == (3, 3, 9)
+        assert np.array_equal(np.frombuffer(raw[16:], dtype="<f8").reshape(3, 3),
+                              np.loadtxt(str(outs["csv"] / "field_p1_r1.csv"), delimiter=","))
+
+    def test_http_grf_matches_api(self, client):
+        r = client.post("/grf", json={"params": [[1.0, 2.0, 1.0, 1.0, 0.0]],
+                                      "grid": {"ncell_x": 3, "ncell_y": 3, "cell_size": 1.0},
+                                      "n_realizations": 2, "streams": payload(16),
+                                      "work_grid": [4, 4]})
+        assert r.status_code == 200
+        fields = np.array(r.json()["fields"])
+        direct = sf.simulate_grf([sf.MaternParams(1.0, 2.0, 1.0)], sf.GridSpec(3, 3, 1.0), 2,
+                                 sf.create_streams(sf.set_base_creator(), 16)[0],
+                                 sf.WorkGrid(4, 4))
+        assert fields.shape == (1, 2, 3, 3) and np.array_equal(fields, direct)
+
+    def test_http_grf_invalid_params_422(self, client):
+        r = client.post("/grf", json={"params": [[-1.0, 2.0, 1.0, 1.0, 0.0]],
+                                      "grid": {"ncell_x": 2, "ncell_y": 2, "cell_size": 1.0},
+                                      "streams": payload(4), "work_grid": [2, 2]})
+        assert r.status_code == 422
