@@ -351,6 +351,27 @@ def stream_io(api, n=1 << 20):
             "file_bytes": size, "dir": d or "tmp"}
 
 
+GRF_BATCH = [(1.0, 8.0, 1.0, 1.0, 0.0), (1.5, 12.0, 2.0, 2.0, 0.5), (0.5, 6.0, 1.5, 1.0, 0.0),
+             (2.0, 10.0, 1.0, 1.5, 1.0)]
+
+
+def run_grf(api, steps):
+    """simulate_grf on the reference's acceptance-11 batch
+    (four Matern parameter sets on a 90 x 57 grid -> four 5130 x 5130
+    covariance blocks, LDL^T, 2 realisations), through `api` (this package or
+    the reference).  Seconds per call, best of `steps`."""
+    best = None
+    for _ in range(steps):
+        st = api.create_streams(api.set_base_creator(), 64)[0]
+        t0 = time.perf_counter()
+        f = api.simulate_grf([api.MaternParams(*p) for p in GRF_BATCH], api.GridSpec(90, 57, 1.0),
+                             2, st, api.WorkGrid(8, 8))
+        dt = time.perf_counter() - t0
+        assert f.shape == (4, 2, 57, 90)
+        best = dt if best is None else min(best, dt)
+    return best
+
+
 def cpu_uniform_sample(orc, rows, threads=0):
     """C5 rows [0, rows) -- every item, rows/g0 owned rows each -- on the oracle."""
     c = C5
@@ -451,6 +472,9 @@ def reference_arm(args, rank, world):
         import streamforge as ref_api
 
         line["workloads"]["stream_io_2p20"] = stream_io(ref_api)
+        s_grf = run_grf(ref_api, 1)
+        line["workloads"]["grf_4x5130"] = {"value": 1.0 / s_grf, "unit": "GRF batches/s",
+                                           "seconds": s_grf}
     except Exception as e:  # noqa: BLE001
         line["workloads"]["stream_io_2p20"] = {"unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
@@ -674,6 +698,14 @@ def main():
                                            counts=c4["counts_last"],
                                            config="configs[3]/C4: T10, 1e10 -> 10001317888 "
                                                   "tables on grid (2048,1024), 2^21 streams")
+    if args.only is None and rank == 0:
+        run_grf(sf, 1)  # warm-up (cuSOLVER workspaces, kernels)
+        s_grf = run_grf(sf, 3)
+        workloads["grf_4x5130"] = dict(value=1.0 / s_grf, unit="GRF batches/s",
+                                       ms_per_step=1e3 * s_grf,
+                                       config="SURVEY 8(f) item 4: simulate_grf, 4 Matern sets "
+                                              "on a 90x57 grid (4 x 5130^2 LDL^T), 2 "
+                                              "realisations, host fields out (best of 3)")
     e2e = run_uniform_e2e(torch, sf, rank, world, min(args.steps, 3), C5)
     if args.only in (None, "fisher") and world == 1:
         fe = run_fisher_e2e(torch, sf, 3, T4, 10 ** 6, (256, 64))
