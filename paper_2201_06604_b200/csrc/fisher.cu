@@ -425,7 +425,8 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
 
     // chunking: enough units to fill the machine, bounded by kMaxChunks
     const int64_t F = (int64_t)(nr - 1) * (nc - 1);
-    constexpr int64_t kTarget = 148LL * 2048 * 2;
+    // units to aim for, in quarters of 148 x 2048 x 2 (tuning knob)
+    const int64_t kTarget = 148LL * 2048 * 2 * tune_knob("SFB_FISHER_TARGET_Q", 4) / 4;
     int64_t nchunks = std::min<int64_t>({(int64_t)kMaxChunks, reps, ceil_div(kTarget, nloc)});
     if (F == 0) nchunks = 1;  // degenerate tables consume no draws
     nchunks = std::max<int64_t>(1, nchunks);
