@@ -720,7 +720,7 @@ def main():
         w["roofline"] = {"bound": "hbm", "achieved": w["gbs"], "unit": "GB/s",
                          "peak_copy": peak, "frac_copy": w["gbs"] / peak,
                          "peak_write": wpeak, "frac_write": w["gbs"] / wpeak,
-                         "note": "compute/issue bound: float32 form box_muller_pair_f32, ~91 SASS (30 FP64, 6 XU) per normal pair incl. 2 MRG31k3p steps"}
+                         "note": "compute/issue bound: float32 form box_muller_pair_f32, ~88 SASS (30 FP64, 6 XU) per normal pair incl. 2 MRG31k3p steps"}
     for key, fops, pk in (("fisher_T4_1e6", FOPS["T4"], "pipes_fisher4"),
                           ("fisher_T10", FOPS["T10"], "pipes_fisher10")):
         if key in workloads:

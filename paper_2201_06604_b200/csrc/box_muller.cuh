@@ -208,17 +208,19 @@ SFB_BM_COLD F32Pair box_muller_pair_f32_exact(uint32_t z1m1, uint32_t z2m1,
     return F32Pair{(float)da, (float)db};
 }
 
+// z2 within kBmExactWin of a multiple of 2^30 (theta near 0, pi, 2 pi): the
+// pair must take the exact form
+SFB_EXP_HD bool bm_f32_needs_exact(uint32_t z2m1) {
+    return ((z2m1 + 1u + kBmExactWin) & ((1u << 30) - 1u)) < 2u * kBmExactWin;
+}
+
+// the fast form without the exact fallback (callers test bm_f32_needs_exact;
+// keeping the rare branch out of this function lets the compiler interleave
+// several pairs in one basic block)
 template <int NEWTON, typename SEED = RsqrtSeedHw>
-SFB_EXP_HD void box_muller_pair_f32(uint32_t z1m1, uint32_t z2m1, const BmPair *logp,
-                                    const BmPair *trigp, const double *angle,
-                                    const uint64_t *logw, const uint64_t *trigw, float &a,
-                                    float &b, const SEED &seed = SEED()) {
-    if (((z2m1 + 1u + kBmExactWin) & ((1u << 30) - 1u)) < 2u * kBmExactWin) {
-        const F32Pair p = box_muller_pair_f32_exact(z1m1, z2m1, logw, trigw);  // theta ~ 0, pi, 2pi
-        a = p.a;
-        b = p.b;
-        return;
-    }
+SFB_EXP_HD void box_muller_pair_f32_core(uint32_t z1m1, uint32_t z2m1, const BmPair *logp,
+                                         const BmPair *trigp, const double *angle, float &a,
+                                         float &b, const SEED &seed = SEED()) {
     const double d = (double)(z1m1 + 1u);  // exact
     const uint64_t bits = as_u64(d);
     const int k = (int)(bits >> 52) - 1053;
@@ -251,6 +253,20 @@ SFB_EXP_HD void box_muller_pair_f32(uint32_t z1m1, uint32_t z2m1, const BmPair *
     const double sin_t = fma_rn(cs.y, cm1, fma_rn(cs.x, sb, cs.y));
     a = (float)(R * cos_t);
     b = (float)(R * sin_t);
+}
+
+template <int NEWTON, typename SEED = RsqrtSeedHw>
+SFB_EXP_HD void box_muller_pair_f32(uint32_t z1m1, uint32_t z2m1, const BmPair *logp,
+                                    const BmPair *trigp, const double *angle,
+                                    const uint64_t *logw, const uint64_t *trigw, float &a,
+                                    float &b, const SEED &seed = SEED()) {
+    if (bm_f32_needs_exact(z2m1)) {
+        const F32Pair p = box_muller_pair_f32_exact(z1m1, z2m1, logw, trigw);  // theta ~ 0, pi, 2pi
+        a = p.a;
+        b = p.b;
+        return;
+    }
+    box_muller_pair_f32_core<NEWTON>(z1m1, z2m1, logp, trigp, angle, a, b, seed);
 }
 
 }  // namespace sfb

@@ -325,6 +325,40 @@ __device__ __forceinline__ void bm(uint32_t z1, uint32_t z2, const BmView &v, fl
     }
 }
 
+// N pairs at once: for the float32 fast form the (rare, ~1e-5) exact fallback
+// is applied after all N pairs are computed, so the hot part is one basic
+// block and the compiler can interleave the N independent FP64 chains
+template <bool FAST, int N>
+__device__ __forceinline__ void bmN(const uint32_t *z1, const uint32_t *z2, const BmView &v,
+                                    double *a, double *b) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) box_muller_pair(z1[k], z2[k], v.logw, v.trigw, a[k], b[k]);
+}
+template <bool FAST, int N>
+__device__ __forceinline__ void bmN(const uint32_t *z1, const uint32_t *z2, const BmView &v,
+                                    float *a, float *b) {
+    if (!FAST) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) bm<false>(z1[k], z2[k], v, a[k], b[k]);
+        return;
+    }
+    bool rare = false;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        box_muller_pair_f32_core<kBmF32Newton>(z1[k], z2[k], v.logp, v.trigp, v.angle, a[k], b[k]);
+        rare |= bm_f32_needs_exact(z2[k]);
+    }
+    if (rare) {
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if (bm_f32_needs_exact(z2[k])) {
+                const F32Pair p = box_muller_pair_f32_exact(z1[k], z2[k], v.logw, v.trigw);
+                a[k] = p.a;
+                b[k] = p.b;
+            }
+    }
+}
+
 // normal, generic layout: unit = (pair, chunk of pair-iterations)
 template <typename T, bool FAST>
 __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__ cur,
@@ -411,13 +445,13 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
                 uint32_t z[4][3];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) step3(st[k], z[k][0], z[k][1], z[k][2]);
+                T a[6], b[6];
+                const uint32_t u1[6] = {z[0][0], z[2][0], z[0][1], z[2][1], z[0][2], z[2][2]};
+                const uint32_t u2[6] = {z[1][0], z[3][0], z[1][1], z[3][1], z[1][2], z[3][2]};
+                bmN<FAST, 6>(u1, u2, bv, a, b);
 #pragma unroll
-                for (int t = 0; t < 3; ++t) {
-                    T a0, b0, a1, b1;
-                    bm<FAST>(z[0][t], z[1][t], bv, a0, b0);
-                    bm<FAST>(z[2][t], z[3][t], bv, a1, b1);
-                    put4(p + g.g1 * (q + t), a0, b0, a1, b1);
-                }
+                for (int t = 0; t < 3; ++t)
+                    put4(p + g.g1 * (q + t), a[2 * t], b[2 * t], a[2 * t + 1], b[2 * t + 1]);
             }
             for (; q < niter; ++q) {
                 T a0, b0, a1, b1;
@@ -436,16 +470,14 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
             T *p = out + (i + g.g0 * rho) * g.npad + j0;
             int64_t q = 0;
             for (; q + 3 <= nfull; q += 3) {
-                uint32_t x0, x1, x2, y0, y1, y2;
-                step3(st[0], x0, x1, x2);
-                step3(st[1], y0, y1, y2);
-                T a, b;
-                bm<FAST>(x0, y0, bv, a, b);
-                put2(p + g.g1 * q, a, b);
-                bm<FAST>(x1, y1, bv, a, b);
-                put2(p + g.g1 * (q + 1), a, b);
-                bm<FAST>(x2, y2, bv, a, b);
-                put2(p + g.g1 * (q + 2), a, b);
+                uint32_t x[3], y[3];
+                step3(st[0], x[0], x[1], x[2]);
+                step3(st[1], y[0], y[1], y[2]);
+                T a[3], b[3];
+                bmN<FAST, 3>(x, y, bv, a, b);
+                put2(p + g.g1 * q, a[0], b[0]);
+                put2(p + g.g1 * (q + 1), a[1], b[1]);
+                put2(p + g.g1 * (q + 2), a[2], b[2]);
             }
             for (; q < nfull; ++q) {
                 T a, b;
