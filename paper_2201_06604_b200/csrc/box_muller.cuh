@@ -106,11 +106,29 @@ SFB_EXP_HD double rounding_error_minus_halfpi(double theta, double thb) {
     return (thb + a) + b;
 }
 
+// sqrt of a positive normal double without the special-case branch of the
+// library sqrt (which splits the unrolled pair loop into separate basic
+// blocks): rsqrt.approx seed (MUFU.RSQ64H, <= 2^-20), one Newton step on
+// 1/sqrt(x) and one residual-corrected step on sqrt(x) -- within an ulp of the
+// correctly rounded root.  The host uses libm sqrt.
+SFB_EXP_HD double sqrt_pos(double x) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = fma_rn(fma_rn(-hx, y * y, 0.5), y, y);  // y (1.5 - x y^2 / 2)
+    const double s = x * y;
+    return fma_rn(fma_rn(-s, s, x), 0.5 * y, s);
+#else
+    return sqrt(x);
+#endif
+}
+
 // the pair transform; z1m1 = z1 - 1, z2m1 = z2 - 1 (see step_m1)
 SFB_EXP_HD void box_muller_pair(uint32_t z1m1, uint32_t z2m1, const uint64_t *logtab,
                                 const uint64_t *trigtab, double &a, double &b) {
     const double ln_u1 = log_u31(z1m1 + 1u, logtab);
-    const double radius = sqrt(SFB_BMC(kC_Neg2) * ln_u1);
+    const double radius = sqrt_pos(SFB_BMC(kC_Neg2) * ln_u1);
     // theta = fl((2 pi NORM) * z2) == fma(c, z2 - 1, c): exact product + c, one rounding
     const double c = SFB_BMC(kC_TwoPiNorm);
     const double theta = fma_rn(c, (double)z2m1, c);

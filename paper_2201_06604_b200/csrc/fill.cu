@@ -503,12 +503,12 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
 // host-side launch planning
 
 constexpr int kThreads = 256;
-// measured on B200 (tools/tune.py normal): float32 fast form best at 3
-// CTAs/SM with one pair per thread (variant 10), float64 at 4 CTAs/SM with
-// one pair per thread (variant 3); the spread over all variants is ~8 %
+// measured on B200 (tools/tune.py normal): both output types are best at 3
+// CTAs/SM with one pair per thread (variant 10); the spread over all
+// variants is ~10 %
 template <typename T>
 constexpr int normal_variant_default() {
-    return sizeof(T) == 4 ? 10 : 3;
+    return 10;
 }
 // enough units to fill 148 SMs several times over (2048 resident threads/SM)
 constexpr int64_t kTargetUnits = 148LL * 2048 * 3;
