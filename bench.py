@@ -684,6 +684,14 @@ def main():
                                        fp64_ops_per_table=FOPS["T10"],
                                        config=f"configs[3]/C4 shape: T10 sparse 10x10 on grid "
                                               f"(2048,1024), {f10['sim_num']} tables per step")
+    if args.only is None:
+        ex = run_uniform(torch, sf, rank, world, max(3, args.steps // 2), args.warmup, C5,
+                         kind="exponential")
+        workloads["rexpGpu_C5"] = dict(value=ex["value"], unit="exponentials/s",
+                                       ms_per_step=ex["ms_per_step"],
+                                       gbs=ex["alg_bytes"] / (ex["launch_ms"] / 1e3) / 1e9,
+                                       config="SURVEY 8(f) item 1: fill_exponential (rate 1) on "
+                                              "the C5 layout, bit-exact glibc log1p port")
     if args.only is None and rank == 0:
         workloads["stream_io_2p20"] = dict(stream_io(sf), config="configs[4] host side: "
                                            "create / save_streams_atomic / load_streams of "

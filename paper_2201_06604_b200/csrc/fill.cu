@@ -57,17 +57,31 @@ __device__ __forceinline__ double u01(uint32_t zm1) {
     return __fma_rn(m, kNorm, kNorm - 0x1p21);
 }
 
+// the exponential rate with its correctly rounded reciprocal (host-computed):
+// v / rate = q0 + (v - rate q0) y with q0 = RN(v y) is RN(v / rate) when
+// y = RN(1 / rate) (Markstein; no over/underflow: used for rates in
+// [2^-500, 2^500], otherwise the IEEE division)
+struct RateArg {
+    double r, y;
+    int markstein;
+};
+
+// -log1p(-u) / rate (_kernels.py:74): glibc log1p port (bit-exact) with its
+// divisions on the branch-free fast path (operands always normal here)
 template <int KIND>
-__device__ __forceinline__ double real_value(uint32_t zm1, double rate) {
+__device__ __forceinline__ double real_value(uint32_t zm1, const RateArg &rate) {
     const double u = u01(zm1);
     if (KIND == kUniform) return u;
-    return __ddiv_rn(-glibc_log1p(-u), rate);  // _kernels.py:74, glibc log1p port: bit-exact
+    const double v = -glibc_log1p(-u, DivFastNormal());
+    if (!rate.markstein) return __ddiv_rn(v, rate.r);
+    const double q0 = v * rate.y;
+    return __fma_rn(__fma_rn(-q0, rate.r, v), rate.y, q0);
 }
 
 // one 16-byte streaming store of a column pair / one 8-byte store
 template <int KIND>
 __device__ __forceinline__ void put_pair(void *out, int64_t off, uint32_t za, uint32_t zb,
-                                         double rate) {
+                                         const RateArg &rate) {
     if (KIND == kInteger)
         __stcs((longlong2 *)((long long *)out + off),
                make_longlong2((long long)za + 1, (long long)zb + 1));
@@ -77,7 +91,8 @@ __device__ __forceinline__ void put_pair(void *out, int64_t off, uint32_t za, ui
 }
 
 template <int KIND>
-__device__ __forceinline__ void put_one(void *out, int64_t off, uint32_t za, double rate) {
+__device__ __forceinline__ void put_one(void *out, int64_t off, uint32_t za,
+                                        const RateArg &rate) {
     if (KIND == kInteger)
         __stcs((long long *)out + off, (long long)za + 1);
     else
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict_
                                                             void *__restrict__ out, Geom g,
                                                             int64_t item_lo, int64_t nloc,
                                                             int64_t chunk, int64_t nunits,
-                                                            double rate, const __grid_constant__ Pow2Table tab) {
+                                                            RateArg rate, const __grid_constant__ Pow2Table tab) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t w = item_lo + u % nloc;
@@ -127,7 +142,7 @@ __global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(int64_t *__restric
                                                          void *__restrict__ out, Geom g,
                                                          int64_t j_lo, int64_t npairs,
                                                          int64_t rows_per_chunk, int64_t nunits,
-                                                         double rate, const __grid_constant__ Pow2Table tab) {
+                                                         RateArg rate, const __grid_constant__ Pow2Table tab) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t jp = u % npairs;
@@ -180,14 +195,14 @@ __device__ __forceinline__ void st256(void *p, uint64_t a, uint64_t b, uint64_t 
 }
 
 template <int KIND>
-__device__ __forceinline__ uint64_t value_bits(uint32_t zm1, double rate) {
+__device__ __forceinline__ uint64_t value_bits(uint32_t zm1, const RateArg &rate) {
     if (KIND == kInteger) return (uint64_t)zm1 + 1u;
     return (uint64_t)__double_as_longlong(real_value<KIND>(zm1, rate));
 }
 
 template <int KIND>
 __device__ __forceinline__ void put_quad(void *out, int64_t off, uint32_t z0, uint32_t z1,
-                                         uint32_t z2, uint32_t z3, double rate) {
+                                         uint32_t z2, uint32_t z3, const RateArg &rate) {
     st256((long long *)out + off, value_bits<KIND>(z0, rate), value_bits<KIND>(z1, rate),
           value_bits<KIND>(z2, rate), value_bits<KIND>(z3, rate));
 }
@@ -197,7 +212,7 @@ __global__ void __launch_bounds__(256, MINB) fill_uniform_quad(int64_t *__restri
                                                          void *__restrict__ out, Geom g,
                                                          int64_t j_lo, int64_t nquads,
                                                          int64_t rows_per_chunk, int64_t nunits,
-                                                         double rate, const __grid_constant__ Pow2Table tab) {
+                                                         RateArg rate, const __grid_constant__ Pow2Table tab) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= nunits) return;
     const int64_t jq = u % nquads;
@@ -547,9 +562,10 @@ static int zero_padding(void *out, size_t elsize, int64_t nrow, int64_t ncol, in
 
 template <int KIND>
 static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_lo,
-                          int64_t item_hi, double rate, cudaStream_t st) {
+                          int64_t item_hi, double rate_d, cudaStream_t st) {
     Pow2Table tab;
     pow2_table(&tab);
+    RateArg rate{rate_d, 1.0 / rate_d, rate_d >= 0x1p-500 && rate_d <= 0x1p500 ? 1 : 0};
     const int64_t nloc = item_hi - item_lo;
     if (nloc == 0) return SFB_OK;
     const int64_t twog0 = 2 * g.g0;
