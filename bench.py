@@ -578,7 +578,7 @@ def run_probes(torch, _lib):
     best = None
     st = _lib.stream_handle()
     per_variant = {}
-    for variant in (0, 1):
+    for variant in (0, 1, 2):
         vbest = None
         for _ in range(4):
             tm.start()
@@ -589,7 +589,8 @@ def run_probes(torch, _lib):
         best = vbest if best is None else min(best, vbest)
     out["hbm_write_gbs"] = buf.numel() / (best / 1e3) / 1e9
     out["hbm_write_gbs_by_shape"] = {"grid_stride": per_variant[0],
-                                     "cta_segments": per_variant[1]}
+                                     "cta_segments": per_variant[1],
+                                     "cta_segments_256b": per_variant[2]}
     del buf
     d = torch.zeros(1, dtype=torch.float64, device="cuda")
     blocks, iters = 148 * 8, 4096

@@ -165,7 +165,8 @@ int sfb_probe_rsqrt(const double *d_x, double *d_y, int64_t n, void *stream);
 /* FP64-pipe roofline probe (bench.py): blocks x 256 threads x iters x 8 DFMA */
 int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream);
 /* write-only HBM probe: fills `bytes` (multiple of 16) with 16-byte stores;
- * variant 0 = grid-stride sweep, 1 = per-CTA contiguous segments (fill shape) */
+ * variant 0 = grid-stride sweep, 1 = per-CTA contiguous segments (fill shape),
+ * 2 = per-CTA segments with 32-byte stores */
 int sfb_probe_write(void *d_out, int64_t bytes, int variant, void *stream);
 
 /* ---- test hooks (host execution of the device arithmetic) --------------- */

@@ -58,13 +58,29 @@ __global__ void rsqrt_probe_kernel(const double *x, double *y, int64_t n) {
     if (i < n) y[i] = RsqrtSeedHw()(x[i]);
 }
 
+// variant 2: per-CTA segments with 32-byte stores (STG.E.ENL2.256)
+__global__ void __launch_bounds__(256) write_probe_seg256_kernel(double *out, int64_t n4,
+                                                                 int64_t seg) {
+    const int64_t b0 = (int64_t)blockIdx.x * seg, b1 = min(b0 + seg, n4);
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += 256)
+        asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(out + 4 * i), "d"(1.0),
+                     "d"(2.0), "d"(3.0), "d"(4.0)
+                     : "memory");
+}
+
 }  // namespace sfb
 
 using namespace sfb;
 
 extern "C" int sfb_probe_write(void *d_out, int64_t bytes, int variant, void *stream) {
     const int64_t n = bytes / 16;
-    if (variant == 1) {
+    if (variant == 2) {
+        const int64_t n4 = bytes / 32;
+        const int64_t blocks = 148 * 64;
+        const int64_t seg = (n4 + blocks - 1) / blocks;
+        write_probe_seg256_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+            (double *)d_out, n4, seg);
+    } else if (variant == 1) {
         const int64_t blocks = 148 * 64;
         const int64_t seg = (n + blocks - 1) / blocks;
         write_probe_seg_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
