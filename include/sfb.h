@@ -177,6 +177,9 @@ int sfb_host_step_u32(int64_t *states, int64_t n, int64_t steps, int64_t *z_out)
 double sfb_host_exp(double x);
 /* the device log1p() port (glibc __log1p FMA variant) evaluated on the host */
 double sfb_host_log1p(double x);
+/* test hook: the branch-free log1p of the exponential fill's domain (x = -u);
+ * *rare = 1 where the fill recomputes with the full port */
+double sfb_host_log1p_fill(double x, int *rare);
 /* the device Box-Muller pair transform (box_muller.cuh) evaluated on the host
  * for draws z1[k], z2[k] in [1, m1]: a = R cos(theta), b = R cos(theta - pi/2) */
 int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double *a,

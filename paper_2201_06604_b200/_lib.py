@@ -74,6 +74,7 @@ _SIGS = {
     "sfb_host_step_u32": ([_i64p, _i64, _i64, _i64p], _int),
     "sfb_host_exp": ([ctypes.c_double], ctypes.c_double),
     "sfb_host_log1p": ([ctypes.c_double], ctypes.c_double),
+    "sfb_host_log1p_fill": ([ctypes.c_double, ctypes.POINTER(ctypes.c_int)], ctypes.c_double),
     "sfb_host_box_muller": ([_i64p, _i64p, _i64, _f64p, _f64p], _int),
     "sfb_host_box_muller_f32": ([_i64p, _i64p, _i64, _int, ctypes.c_double, _f32p, _f32p], _int),
     "sfb_host_fisher_replicates": ([_i64p, _i64p, _int, _i64p, _int, _f64p, ctypes.c_double,

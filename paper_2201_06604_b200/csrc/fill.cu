@@ -66,16 +66,49 @@ struct RateArg {
     int markstein;
 };
 
-// -log1p(-u) / rate (_kernels.py:74): glibc log1p port (bit-exact) with its
-// divisions on the branch-free fast path (operands always normal here)
+// -log1p(-u) / rate (_kernels.py:74), bit-exact: log1p_fill_domain (the
+// glibc port without data-dependent branches) for N values at once, the rare
+// inputs of glibc's other paths (~2^-19) recomputed afterwards with the full
+// port out of line, so the N evaluations stay in one basic block; divisions
+// on the branch-free fast path (operands always normal on this domain); the
+// division by the rate is Markstein's correction when RateArg allows it.
+__device__ __noinline__ double log1p_rare(double x) { return glibc_log1p(x, DivFastNormal()); }
+
+template <int KIND, int N>
+__device__ __forceinline__ void real_values(const uint32_t *zm1, const RateArg &rate,
+                                            double *v) {
+    if (KIND == kUniform) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = u01(zm1[k]);
+        return;
+    }
+    bool any = false, rare[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        v[k] = -log1p_fill_domain(-u01(zm1[k]), DivFastNormal(), rare[k]);
+        any |= rare[k];
+    }
+    if (any) {
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if (rare[k]) v[k] = -log1p_rare(-u01(zm1[k]));
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (!rate.markstein) {
+            v[k] = __ddiv_rn(v[k], rate.r);
+        } else {
+            const double q0 = v[k] * rate.y;
+            v[k] = __fma_rn(__fma_rn(-q0, rate.r, v[k]), rate.y, q0);
+        }
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ double real_value(uint32_t zm1, const RateArg &rate) {
-    const double u = u01(zm1);
-    if (KIND == kUniform) return u;
-    const double v = -glibc_log1p(-u, DivFastNormal());
-    if (!rate.markstein) return __ddiv_rn(v, rate.r);
-    const double q0 = v * rate.y;
-    return __fma_rn(__fma_rn(-q0, rate.r, v), rate.y, q0);
+    double v;
+    real_values<KIND, 1>(&zm1, rate, &v);
+    return v;
 }
 
 // one 16-byte streaming store of a column pair / one 8-byte store
@@ -85,9 +118,12 @@ __device__ __forceinline__ void put_pair(void *out, int64_t off, uint32_t za, ui
     if (KIND == kInteger)
         __stcs((longlong2 *)((long long *)out + off),
                make_longlong2((long long)za + 1, (long long)zb + 1));
-    else
-        __stcs((double2 *)((double *)out + off),
-               make_double2(real_value<KIND>(za, rate), real_value<KIND>(zb, rate)));
+    else {
+        const uint32_t z[2] = {za, zb};
+        double v[2];
+        real_values<KIND, 2>(z, rate, v);
+        __stcs((double2 *)((double *)out + off), make_double2(v[0], v[1]));
+    }
 }
 
 template <int KIND>
@@ -194,17 +230,21 @@ __device__ __forceinline__ void st256(void *p, uint64_t a, uint64_t b, uint64_t 
                  : "memory");
 }
 
-template <int KIND>
-__device__ __forceinline__ uint64_t value_bits(uint32_t zm1, const RateArg &rate) {
-    if (KIND == kInteger) return (uint64_t)zm1 + 1u;
-    return (uint64_t)__double_as_longlong(real_value<KIND>(zm1, rate));
-}
 
 template <int KIND>
 __device__ __forceinline__ void put_quad(void *out, int64_t off, uint32_t z0, uint32_t z1,
                                          uint32_t z2, uint32_t z3, const RateArg &rate) {
-    st256((long long *)out + off, value_bits<KIND>(z0, rate), value_bits<KIND>(z1, rate),
-          value_bits<KIND>(z2, rate), value_bits<KIND>(z3, rate));
+    if (KIND == kInteger) {
+        st256((long long *)out + off, (uint64_t)z0 + 1u, (uint64_t)z1 + 1u, (uint64_t)z2 + 1u,
+              (uint64_t)z3 + 1u);
+        return;
+    }
+    const uint32_t z[4] = {z0, z1, z2, z3};
+    double v[4];
+    real_values<KIND, 4>(z, rate, v);
+    st256((long long *)out + off, (uint64_t)__double_as_longlong(v[0]),
+          (uint64_t)__double_as_longlong(v[1]), (uint64_t)__double_as_longlong(v[2]),
+          (uint64_t)__double_as_longlong(v[3]));
 }
 
 template <int KIND, int MINB, bool STEP3 = true>

@@ -639,6 +639,13 @@ double sfb_host_exp(double x) { return glibc_exp(x, kExpTable); }
 
 double sfb_host_log1p(double x) { return glibc_log1p(x); }
 
+double sfb_host_log1p_fill(double x, int *rare) {
+    bool r = false;
+    const double v = log1p_fill_domain(x, DivIeee(), r);
+    *rare = r ? 1 : 0;
+    return v;
+}
+
 int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const int64_t *ncolt,
                                int nc, const double *lf, double threshold, int64_t reps,
                                int64_t item_lo, int64_t item_hi, double *stats,

@@ -150,6 +150,34 @@ def test_log1p_port_bit_exact_against_libm():
     assert not bad, bad[:10]
 
 
+def test_log1p_fill_domain_bit_exact_against_libm():
+    """The branch-free log1p of the exponential fill (x = -u, u = z 2^-31) ==
+    libm log1p bit for bit wherever it does not flag the input as rare, and the
+    rare inputs are exactly glibc's other paths (|x| < 2^-29, hu == 0)."""
+    libm = ctypes.CDLL(ctypes.util.find_library("m"))
+    libm.log1p.argtypes = [ctypes.c_double]
+    libm.log1p.restype = ctypes.c_double
+    port = _lib.lib().sfb_host_log1p_fill
+    rng = np.random.default_rng(9)
+    z = np.concatenate([rng.integers(1, 2 ** 31, 300000), np.arange(1, 4097),
+                        2 ** 31 - np.arange(1, 4097),
+                        # around the k = 0 / k != 0 switch (u = 0.2929) and powers of 2
+                        int(0.29289321881345254 * 2 ** 31) + np.arange(-2000, 2001),
+                        np.concatenate([(2 ** 31 - 2 ** e) + np.arange(-300, 301)
+                                        for e in range(20, 31)])])
+    z = z[(z >= 1) & (z < 2 ** 31)]
+    flag = ctypes.c_int()
+    nrare = 0
+    for zi in z:
+        x = -(float(zi) * 2.0 ** -31)
+        v = port(x, ctypes.byref(flag))
+        if flag.value:
+            nrare += 1
+            continue
+        assert _bits(v) == _bits(libm.log1p(x)), (int(zi), v, libm.log1p(x))
+    assert nrare < 0.02 * len(z)
+
+
 def test_printed_matrix_and_goldens(G):
     s4 = sf.create_streams(sf.set_base_creator(), 4)[0]
     assert np.array_equal(s4.matrix(), PRINTED_STREAM_MATRIX)

@@ -75,15 +75,19 @@ def main():
                         "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
             print(json.dumps(res[-1]), flush=True)
         os.environ.pop("SFB_UNIFORM_VARIANT")
-        for kind in ("exponential", "uniform-integer"):
+        for kind, v in (("exponential", 0), ("exponential", 0x30), ("exponential", 0x40),
+                        ("exponential", 0x4000), ("uniform-integer", 0)):
+            os.environ["SFB_UNIFORM_VARIANT"] = str(v)
             out2 = out.view(torch.int64) if kind == "uniform-integer" else out
 
             def fn2(kind=kind, out2=out2):
                 launch_fill(kind, cur, st.count, out2, 65536, 65536, 65536, 1024, 1024)
 
             ms = timeit(fn2)
-            res.append({"w": f"{kind}_C5", "ms": ms, "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
+            res.append({"w": f"{kind}_C5", "variant": hex(v), "ms": ms,
+                        "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
             print(json.dumps(res[-1]), flush=True)
+        os.environ.pop("SFB_UNIFORM_VARIANT", None)
         os.environ.pop("SFB_UNIFORM_VARIANT", None)
         del out
         torch.cuda.empty_cache()
