@@ -694,6 +694,26 @@ def main():
                                        config="SURVEY 8(f) item 1: fill_exponential (rate 1) on "
                                               "the C5 layout, bit-exact glibc log1p port")
     if args.only is None and rank == 0:
+        # the API's default use (configs[0]/C1 pattern at GPU scale): a 1 x n
+        # vector on the default 64 x 8 grid, i.e. 8 active streams of 512
+        from paper_2201_06604_b200.grid import launch_fill
+
+        st = sf.create_streams(sf.set_base_creator(), 512)[0]
+        vcur = st.device_current()
+        vout = torch.empty((1, 10 ** 8), dtype=torch.float64, device="cuda")
+        tm = Timer(torch)
+        for _ in range(args.warmup):
+            launch_fill("uniform", vcur, st.count, vout, 1, 10 ** 8, 10 ** 8, 64, 8)
+        tm.start()
+        for _ in range(args.steps):
+            launch_fill("uniform", vcur, st.count, vout, 1, 10 ** 8, 10 ** 8, 64, 8)
+        vms = tm.stop() / args.steps
+        workloads["runifGpu_vector_1e8"] = dict(
+            value=1e8 / (vms / 1e3), unit="uniforms/s", ms_per_step=vms,
+            gbs=8e8 / (vms / 1e3) / 1e9,
+            config="configs[0] pattern at GPU scale: FillRequest(shape=1e8) on the default "
+                   "WorkGrid(64,8) -> 8 active streams, generic kernel")
+        del vout
         workloads["stream_io_2p20"] = dict(stream_io(sf), config="configs[4] host side: "
                                            "create / save_streams_atomic / load_streams of "
                                            "2^20 streams (C++ creation chain and stream files)")

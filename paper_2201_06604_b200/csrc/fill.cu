@@ -136,23 +136,36 @@ __device__ __forceinline__ void put_one(void *out, int64_t off, uint32_t za,
 }
 
 // ---------------------------------------------------------------------------
+// generic layouts (odd g1, vectors, ragged shards): unit = (grid row i, chunk
+// c of an item's draws, column index jj), jj fastest -- adjacent lanes are the
+// items that write adjacent columns, and only items with owned cells get
+// units (a 1 x n vector on the default 64 x 8 grid has 8 active items)
+struct GenMap {
+    int64_t lo, hi;      // shard: items (uniform kinds) / pairs (normal)
+    int64_t jlo, J;      // column indices covered: items' j / pairs' jp
+    int64_t i_lo;        // first active grid row; rows i_lo .. (nunits / (J nchunks))
+    int64_t nchunks, chunk, nunits;
+};
+
 // uniform kinds, generic layout
 template <int KIND>
 __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict__ cur,
                                                             void *__restrict__ out, Geom g,
-                                                            int64_t item_lo, int64_t nloc,
-                                                            int64_t chunk, int64_t nunits,
-                                                            RateArg rate, const __grid_constant__ Pow2Table tab) {
+                                                            GenMap m, RateArg rate,
+                                                            const __grid_constant__ Pow2Table tab) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= nunits) return;
-    const int64_t w = item_lo + u % nloc;
-    const int64_t c = u / nloc;
-    const int64_t i = w % g.g0, j = w / g.g0;
+    if (u >= m.nunits) return;
+    const int64_t j = m.jlo + u % m.J;
+    const int64_t r = u / m.J;
+    const int64_t c = r % m.nchunks;
+    const int64_t i = m.i_lo + r / m.nchunks;
+    const int64_t w = i + g.g0 * j;
+    if (w < m.lo || w >= m.hi) return;
     const int64_t nr = owned(g.nrow, i, g.g0), nc = owned(g.ncol, j, g.g1);
     const int64_t total = nr * nc;
-    const int64_t d0 = c * chunk;
+    const int64_t d0 = c * m.chunk;
     if (d0 >= total) return;
-    const int64_t d1 = min(d0 + chunk, total);
+    const int64_t d1 = min(d0 + m.chunk, total);
     Mrg s = load_state(cur + 6 * w);
     skip(tab, s, (uint64_t)d0);
     int64_t rho = d0 / nc, q = d0 % nc;
@@ -417,25 +430,27 @@ __device__ __forceinline__ void bmN(const uint32_t *z1, const uint32_t *z2, cons
 // normal, generic layout: unit = (pair, chunk of pair-iterations)
 template <typename T, bool FAST>
 __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__ cur,
-                                                           T *__restrict__ out, Geom g,
-                                                           int64_t pair_lo, int64_t nloc,
-                                                           int64_t chunk, int64_t nunits,
+                                                           T *__restrict__ out, Geom g, GenMap m,
                                                            const __grid_constant__ Pow2Table tab) {
     __shared__ __align__(16) unsigned char bm_raw[kBmSmemBytes];
     const BmView bv = stage_bm_tables<FAST && sizeof(T) == 4>(bm_raw);
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= nunits) return;
-    const int64_t p = pair_lo + u % nloc;
-    const int64_t c = u / nloc;
+    if (u >= m.nunits) return;
     const int64_t half = g.g1 / 2;
-    const int64_t i = p / half, j0 = 2 * (p % half);  // _kernels.py:125-128
+    const int64_t jp = m.jlo + u % m.J;
+    const int64_t r = u / m.J;
+    const int64_t c = r % m.nchunks;
+    const int64_t i = m.i_lo + r / m.nchunks;
+    const int64_t p = i * half + jp;
+    if (p < m.lo || p >= m.hi) return;
+    const int64_t j0 = 2 * jp;  // _kernels.py:125-128
     const int64_t s0 = i * g.g1 + j0;
     const int64_t nr = owned(g.nrow, i, g.g0);
     const int64_t niter = owned(g.ncol, j0, g.g1);  // `while ca < ncol` trips per row
     const int64_t total = nr * niter;
-    const int64_t d0 = c * chunk;
+    const int64_t d0 = c * m.chunk;
     if (d0 >= total) return;
-    const int64_t d1 = min(d0 + chunk, total);
+    const int64_t d1 = min(d0 + m.chunk, total);
     Mrg sa = load_state(cur + 6 * s0), sb = load_state(cur + 6 * (s0 + 1));
     skip(tab, sa, (uint64_t)d0);
     skip(tab, sb, (uint64_t)d0);
@@ -702,12 +717,23 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
         }
         return launch_check("fill_uniform_fast");
     }
+    // items with owned cells: rows i < min(g0, nrow), columns j < min(g1, ncol)
+    GenMap m{};
+    m.lo = item_lo;
+    m.hi = item_hi;
+    m.i_lo = 0;
+    const int64_t ieff = std::min(g.g0, g.nrow);
+    const int64_t jeff = std::min(g.g1, g.ncol);
+    m.jlo = item_lo / g.g0;
+    m.J = std::min(jeff, (item_hi - 1) / g.g0 + 1) - m.jlo;
+    if (m.J <= 0) return SFB_OK;
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
-    int64_t chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * nloc, kTargetUnits));
-    chunk = std::min(chunk, std::max<int64_t>(1, maxdraws));
-    const int64_t nunits = nloc * ceil_div(maxdraws, chunk);
-    fill_uniform_generic<KIND><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
-        cur, out, g, item_lo, nloc, chunk, nunits, rate, tab);
+    m.chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * ieff * m.J, kTargetUnits));
+    m.chunk = std::min(m.chunk, std::max<int64_t>(1, maxdraws));
+    m.nchunks = ceil_div(maxdraws, m.chunk);
+    m.nunits = ieff * m.J * m.nchunks;
+    fill_uniform_generic<KIND><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0, st>>>(
+        cur, out, g, m, rate, tab);
     return launch_check("fill_uniform_generic");
 }
 
@@ -780,16 +806,35 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
             launch_normal_fast<T, true>(use_two, minb, st, cur, out, g, i_lo, nrows_grid, rpc, nu);
         return launch_check("fill_normal_fast");
     }
+    // pairs with owned cells: grid rows of the shard below min(g0, nrow),
+    // pair columns jp with 2 jp < ncol
+    GenMap m{};
+    m.lo = pair_lo;
+    m.hi = pair_hi;
+    m.i_lo = pair_lo / half;
+    const int64_t i_end = std::min((pair_hi - 1) / half + 1, std::min(g.g0, g.nrow));
+    if (i_end <= m.i_lo) return SFB_OK;
+    const int64_t jpeff = std::min(half, ceil_div(g.ncol, 2));
+    if (i_end - m.i_lo == 1) {  // a shard inside one grid row
+        m.jlo = pair_lo - m.i_lo * half;
+        m.J = std::min(jpeff, pair_hi - m.i_lo * half) - m.jlo;
+    } else {
+        m.jlo = 0;
+        m.J = jpeff;
+    }
+    if (m.J <= 0) return SFB_OK;
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
-    int64_t chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * nloc, kTargetUnits));
-    chunk = std::min(chunk, std::max<int64_t>(1, maxdraws));
-    const int64_t nunits = nloc * ceil_div(maxdraws, chunk);
+    m.chunk = std::max(kMinChunkDraws,
+                       ceil_div(maxdraws * (i_end - m.i_lo) * m.J, kTargetUnits));
+    m.chunk = std::min(m.chunk, std::max<int64_t>(1, maxdraws));
+    m.nchunks = ceil_div(maxdraws, m.chunk);
+    m.nunits = (i_end - m.i_lo) * m.J * m.nchunks;
     if (tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>()) & 4)
-        fill_normal_generic<T, false><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
-            cur, out, g, pair_lo, nloc, chunk, nunits, tab);
+        fill_normal_generic<T, false><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0,
+                                         st>>>(cur, out, g, m, tab);
     else
-        fill_normal_generic<T, true><<<(unsigned)ceil_div(nunits, kThreads), kThreads, 0, st>>>(
-            cur, out, g, pair_lo, nloc, chunk, nunits, tab);
+        fill_normal_generic<T, true><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0,
+                                        st>>>(cur, out, g, m, tab);
     return launch_check("fill_normal_generic");
 }
 

@@ -91,6 +91,21 @@ def main():
         os.environ.pop("SFB_UNIFORM_VARIANT", None)
         del out
         torch.cuda.empty_cache()
+    if "vector" in what:  # the API's default use: a 1 x n vector on the default 64 x 8 grid
+        st = sf.create_streams(sf.set_base_creator(), 512)[0]
+        cur = st.device_current()
+        n = 10 ** 8
+        for kind, dt in (("uniform", torch.float64), ("normal", torch.float64),
+                         ("normal", torch.float32), ("exponential", torch.float64)):
+            out = torch.empty((1, n), dtype=dt, device="cuda")
+
+            def fnv(kind=kind, out=out):
+                launch_fill(kind, cur, st.count, out, 1, n, n, 64, 8)
+
+            ms = timeit(fnv)
+            res.append({"w": f"vector_{kind}_{str(dt)[6:]}", "ms": ms, "per_s": n / (ms / 1e3),
+                        "gbs": n * out.element_size() / (ms / 1e3) / 1e9})
+            print(json.dumps(res[-1]), flush=True)
     if "normal" in what:
         for dt in (torch.float32, torch.float64):
             fn = normal_case(dt)
