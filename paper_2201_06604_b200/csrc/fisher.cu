@@ -26,6 +26,7 @@
 // reduced warp-shuffle -> shared memory -> one 64-bit atomic per CTA; the
 // multi-GPU layer then does one NCCL all-reduce of that count.
 #include <cuda_runtime.h>
+#include <string.h>
 
 #include <algorithm>
 #include <atomic>
@@ -39,15 +40,19 @@
 
 namespace sfb {
 
-constexpr int kMaxChunks = 96;
+constexpr int kMaxChunks = 96;        // chunk jumps in the small parameter block
+constexpr int kMaxChunksLarge = 384;  // small grids (e.g. the default 64 x 16): 27 KB block
 constexpr int kFisherWalkDefault = 1;  // fisher_sampler.cuh walk form (tools/tune.py)
 constexpr int kFisherThreads = 256;
 constexpr int kMaxFisherSmem = 200 * 1024;
 static const uint64_t kHostExpTab[256] = SFB_EXP_TABLE_INIT;
 
-struct ChunkJumps {
-    Jump j[kMaxChunks];
+template <int N>
+struct ChunkJumpsN {
+    Jump j[N];
 };
+using ChunkJumps = ChunkJumpsN<kMaxChunks>;
+using ChunkJumpsLarge = ChunkJumpsN<kMaxChunksLarge>;
 
 struct FisherArgs {
     int64_t *cur;
@@ -75,9 +80,9 @@ struct LfGlobal {
 using LfShared = LfPlain;
 
 // dynamic shared memory: exp table (2 KiB) | margins | [lf] | jwork
-template <bool LF_SMEM, int MINB, int WALK>
+template <bool LF_SMEM, int MINB, int WALK, typename JUMPS = ChunkJumps>
 __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const FisherArgs a,
-                                                         const __grid_constant__ ChunkJumps jumps) {
+                                                         const __grid_constant__ JUMPS jumps) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *exptab = (uint64_t *)smem;
     int32_t *rowm = (int32_t *)(exptab + 256);
@@ -371,6 +376,25 @@ static cudaError_t launch_fisher_walk(unsigned blocks, size_t smem, cudaStream_t
 }
 
 template <bool LF_SMEM, int MINB>
+static cudaError_t launch_fisher_large(unsigned blocks, size_t smem, cudaStream_t st,
+                                       const FisherArgs &a, const ChunkJumpsLarge &jumps) {
+    static std::atomic<uint64_t> done_mask{0};
+    int d = 0;
+    cudaGetDevice(&d);
+    const uint64_t bit = 1ull << (d & 63);
+    if (!(done_mask.load() & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(
+            fisher_kernel<LF_SMEM, MINB, kFisherWalkDefault, ChunkJumpsLarge>,
+            cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxFisherSmem);
+        if (e != cudaSuccess) return e;
+        done_mask.fetch_or(bit);
+    }
+    fisher_kernel<LF_SMEM, MINB, kFisherWalkDefault, ChunkJumpsLarge>
+        <<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    return cudaGetLastError();
+}
+
+template <bool LF_SMEM, int MINB>
 static cudaError_t launch_fisher(unsigned blocks, size_t smem, cudaStream_t st,
                                  const FisherArgs &a, const ChunkJumps &jumps) {
     switch (tune_knob("SFB_FISHER_WALK", kFisherWalkDefault)) {
@@ -427,17 +451,21 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     const int64_t F = (int64_t)(nr - 1) * (nc - 1);
     // units to aim for, in quarters of 148 x 2048 x 2 (tuning knob)
     const int64_t kTarget = 148LL * 2048 * 2 * tune_knob("SFB_FISHER_TARGET_Q", 4) / 4;
-    int64_t nchunks = std::min<int64_t>({(int64_t)kMaxChunks, reps, ceil_div(kTarget, nloc)});
+    int64_t nchunks = std::min<int64_t>({(int64_t)kMaxChunksLarge, reps, ceil_div(kTarget, nloc)});
     if (F == 0) nchunks = 1;  // degenerate tables consume no draws
     nchunks = std::max<int64_t>(1, nchunks);
     const int64_t rpc = ceil_div(reps, nchunks);
     nchunks = ceil_div(reps, rpc);
-    ChunkJumps jumps;
-    // J_c = A^(c rpc F): one exact power, then one product per chunk
+    // J_c = A^(c rpc F): one exact power, then one product per chunk; up to
+    // kMaxChunks in the small parameter block, else the large one
+    thread_local ChunkJumpsLarge jl;
     Jump step;
     jump_pow((uint64_t)(rpc * F), &step);
-    jump_pow(0, &jumps.j[0]);
-    for (int64_t c = 1; c < nchunks; ++c) jump_mul(jumps.j[c - 1], step, &jumps.j[c]);
+    jump_pow(0, &jl.j[0]);
+    for (int64_t c = 1; c < nchunks; ++c) jump_mul(jl.j[c - 1], step, &jl.j[c]);
+    const bool large = nchunks > kMaxChunks;
+    ChunkJumps jumps;
+    if (!large) memcpy(jumps.j, jl.j, sizeof(Jump) * (size_t)nchunks);
 
     FisherArgs a;
     a.cur = d_cur;
@@ -480,7 +508,10 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     // register cap: 4 CTAs/SM (64 regs) -- best for every table measured on
     // B200 (tools/tune.py sweep of 3 walk forms x {3, 4} CTAs/SM)
     const int minb = tune_knob("SFB_FISHER_MINB", 4);
-    if (lf_smem) {
+    if (large) {
+        e = lf_smem ? launch_fisher_large<true, 4>(blocks, smem, st, a, jl)
+                    : launch_fisher_large<false, 4>(blocks, smem, st, a, jl);
+    } else if (lf_smem) {
         if (minb >= 4)
             e = launch_fisher<true, 4>(blocks, smem, st, a, jumps);
         else if (minb == 3)

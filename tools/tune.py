@@ -124,7 +124,9 @@ def main():
         for name, table, n, g in (("T4", T4, 10 ** 6, (256, 64)),
                                   ("T4x16", T4, 16 * 10 ** 6, (2048, 1024)),
                                   ("T10", t10, 1 << 23, (2048, 1024)),
-                                  ("month", month, 1 << 22, (2048, 1024))):
+                                  ("month", month, 1 << 22, (2048, 1024)),
+                                  ("T4_default_grid", T4, 10 ** 6, (64, 16)),
+                                  ("month_default_grid", month, 10 ** 6, (64, 16))):
             if name not in only:
                 continue
             sim, fn, cnt = fisher_case(table, n, g)
