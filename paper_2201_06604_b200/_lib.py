@@ -119,14 +119,22 @@ def dptr(t) -> int:
     return t.data_ptr()
 
 
+_DEVICE_OK = False
+
+
 def require_device():
-    """The product path needs an sm_100a GPU; fail loudly otherwise."""
+    """The product path needs an sm_100a GPU; fail loudly otherwise (the
+    positive answer is cached: it is asked on every API call)."""
+    global _DEVICE_OK
+    if _DEVICE_OK:
+        return
     import torch
 
     if not torch.cuda.is_available():
         raise errors.DeviceError("no CUDA device visible: the B200 kernels have no CPU fallback")
     if not lib().sfb_device_ok():
         raise errors.DeviceError("libsfb.so is built for sm_100a only (B200); this device is not")
+    _DEVICE_OK = True
 
 
 def stream_handle():
