@@ -71,3 +71,64 @@ def test_random_layouts_and_splits_match_oracle(lay):
     else:
         err = np.abs(got - ref)
         assert ((err <= 4 * np.spacing(np.abs(ref))) | (err <= 2.0 ** -60)).all(), lay
+
+
+@hs.composite
+def fisher_cases(draw):
+    nr = draw(hs.integers(1, 6))
+    nc = draw(hs.integers(1, 6))
+    if nr * nc < 2:
+        nc = 2
+    scale = draw(hs.sampled_from([2, 10, 60, 400]))
+    table = np.array(draw(hs.lists(hs.integers(0, scale), min_size=nr * nc, max_size=nr * nc)),
+                     dtype=np.int64).reshape(nr, nc)
+    if table.sum() == 0:
+        table[0, 0] = 1
+    g0 = draw(hs.integers(1, 8))
+    g1 = draw(hs.integers(1, 8))
+    reps = draw(hs.integers(1, 40))
+    cuts = sorted(set(draw(hs.lists(hs.integers(0, g0 * g1), max_size=3))) | {0, g0 * g1})
+    memo = draw(hs.sampled_from(["0", "1"]))
+    return table, g0, g1, reps, cuts, memo
+
+
+@settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck))
+@given(fisher_cases())
+def test_random_fisher_tables_and_splits_match_oracle(case):
+    """Random margins (zeros, degenerate rows/columns, wide ranges), grids,
+    replicate counts and item splits, memo on/off: counts, statistics and
+    final states bit for bit."""
+    import os
+
+    import torch
+
+    from paper_2201_06604_b200 import _lib
+
+    table, g0, g1, reps, cuts, memo = case
+    n = g0 * g1
+    rm, cm = table.sum(1), table.sum(0)
+    lf = oa.lf_table(int(table.sum()))
+    thr = oa.relaxed(oa.logfact_sum(table))
+    cur = torch.from_numpy(oa.fresh_states(n)).cuda()
+    stats = torch.empty(n * reps, dtype=torch.float64, device="cuda")
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    os.environ["SFB_FISHER_MEMO"] = memo
+    try:
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            if hi > lo:
+                _lib.check(_lib.lib().sfb_fisher_replicates(
+                    _lib.dptr(cur), n, _lib.ptr(np.ascontiguousarray(rm)), len(rm),
+                    _lib.ptr(np.ascontiguousarray(cm)), len(cm), _lib.ptr(lf, _lib._f64p),
+                    len(lf), thr, reps, lo, hi, _lib.dptr(stats[lo * reps:]), None,
+                    _lib.dptr(count), 0, _lib.stream_handle()))
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("SFB_FISHER_MEMO", None)
+    ref_states = oa.fresh_states(n)
+    ref_stats = np.empty(n * reps)
+    from oracle import oracle as orc
+
+    rc = orc.fisher_replicates(ref_states, rm, cm, lf, thr, reps, n, ref_stats)
+    assert int(count.item()) == rc, case
+    assert np.array_equal(stats.cpu().numpy(), ref_stats), case
+    assert np.array_equal(cur.cpu().numpy(), ref_states), case
