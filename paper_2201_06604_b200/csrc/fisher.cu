@@ -42,7 +42,7 @@ namespace sfb {
 
 constexpr int kMaxChunks = 96;        // chunk jumps in the small parameter block
 constexpr int kMaxChunksLarge = 384;  // small grids (e.g. the default 64 x 16): 27 KB block
-constexpr int kFisherWalkDefault = 1;  // fisher_sampler.cuh walk form (tools/tune.py)
+constexpr int kFisherWalkDefault = 3;  // fisher_sampler.cuh walk form (tools/tune.py)
 constexpr int kFisherThreads = 256;
 constexpr int kMaxFisherSmem = 200 * 1024;
 static const uint64_t kHostExpTab[256] = SFB_EXP_TABLE_INIT;
@@ -400,7 +400,8 @@ static cudaError_t launch_fisher(unsigned blocks, size_t smem, cudaStream_t st,
     switch (tune_knob("SFB_FISHER_WALK", kFisherWalkDefault)) {
         case 0: return launch_fisher_walk<LF_SMEM, MINB, 0>(blocks, smem, st, a, jumps);
         case 2: return launch_fisher_walk<LF_SMEM, MINB, 2>(blocks, smem, st, a, jumps);
-        default: return launch_fisher_walk<LF_SMEM, MINB, 1>(blocks, smem, st, a, jumps);
+        case 1: return launch_fisher_walk<LF_SMEM, MINB, 1>(blocks, smem, st, a, jumps);
+        default: return launch_fisher_walk<LF_SMEM, MINB, 3>(blocks, smem, st, a, jumps);
     }
 }
 

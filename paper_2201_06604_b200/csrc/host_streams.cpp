@@ -661,7 +661,7 @@ int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const
                        kMemoMaxEntries, kMemoMaxSeq, kMemoSigmas);
     const MemoSet ms = hm.view();
     const MemoSet *mp = use_memo ? &ms : nullptr;
-    const int walk = tune_knob("SFB_FISHER_WALK", 1);
+    const int walk = tune_knob("SFB_FISHER_WALK", 3);
     int64_t hits = 0;
     for (int64_t w = item_lo; w < item_hi; ++w) {
         Mrg s = load_state(cur + 6 * w);
@@ -670,6 +670,8 @@ int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const
                 walk == 0 ? sample_table<0>(rowm.data(), colm.data(), nr, nc, (int)ntot,
                                             LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp)
                 : walk == 2 ? sample_table<2>(rowm.data(), colm.data(), nr, nc, (int)ntot,
+                                              LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp)
+                : walk == 3 ? sample_table<3>(rowm.data(), colm.data(), nr, nc, (int)ntot,
                                               LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp)
                             : sample_table<1>(rowm.data(), colm.data(), nr, nc, (int)ntot,
                                               LfPlain{lf}, kExpTable, s, jw.data(), 1, nullptr, mp);

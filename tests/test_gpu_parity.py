@@ -539,7 +539,7 @@ def test_exponential_layouts_bit_exact(shape, g, n, rate):
     assert np.array_equal(st.current, ref_st)
 
 
-@pytest.mark.parametrize("walk", [0, 1, 2])
+@pytest.mark.parametrize("walk", [0, 1, 2, 3])
 def test_fisher_walk_forms_bit_exact(G, A, walk, monkeypatch):
     monkeypatch.setenv("SFB_FISHER_WALK", str(walk))
     for key in ("F_T10_1e6", "F_month_s", "F_Ebig", "F_E5x2"):
