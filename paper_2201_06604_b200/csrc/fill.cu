@@ -60,7 +60,8 @@ __device__ __forceinline__ double u01(uint32_t zm1) {
 // the exponential rate with its correctly rounded reciprocal (host-computed):
 // v / rate = q0 + (v - rate q0) y with q0 = RN(v y) is RN(v / rate) when
 // y = RN(1 / rate) (Markstein; no over/underflow: used for rates in
-// [2^-500, 2^500], otherwise the IEEE division)
+// [2^-500, 2^500], otherwise the IEEE division); markstein == 2: rate 1, no
+// division at all (v / 1 == v)
 struct RateArg {
     double r, y;
     int markstein;
@@ -95,7 +96,8 @@ __device__ __forceinline__ void real_values(const uint32_t *zm1, const RateArg &
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        if (!rate.markstein) {
+        if (rate.markstein == 2) {  // rate 1: v / 1 == v
+        } else if (!rate.markstein) {
             v[k] = __ddiv_rn(v[k], rate.r);
         } else {
             const double q0 = v[k] * rate.y;
@@ -620,7 +622,8 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
                           int64_t item_hi, double rate_d, cudaStream_t st) {
     Pow2Table tab;
     pow2_table(&tab);
-    RateArg rate{rate_d, 1.0 / rate_d, rate_d >= 0x1p-500 && rate_d <= 0x1p500 ? 1 : 0};
+    RateArg rate{rate_d, 1.0 / rate_d,
+                 rate_d == 1.0 ? 2 : rate_d >= 0x1p-500 && rate_d <= 0x1p500 ? 1 : 0};
     const int64_t nloc = item_hi - item_lo;
     if (nloc == 0) return SFB_OK;
     const int64_t twog0 = 2 * g.g0;
@@ -663,7 +666,12 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
             qchunks = ceil_div(rows, qrpc);
             const int64_t qunits = qbase * qchunks;
             const unsigned qb = (unsigned)ceil_div(qunits, kThreads);
-            switch ((v >> 4) & 15) {  // register cap / single-step variants (tuning)
+            // register cap / single-step variants (tuning); the exponential's
+            // twelve log1p evaluations in flight want 3 CTAs/SM (measured 19.4 ->
+            // 15.4 ms on C5), the store-bound kinds the uncapped default
+            int sel = (v >> 4) & 15;
+            if (sel == 0 && KIND == kExponential) sel = 3;
+            switch (sel) {
                 case 3:
                     fill_uniform_quad<KIND, 3><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
                                                                         qrpc, qunits, rate, tab);

@@ -75,8 +75,8 @@ def main():
                         "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
             print(json.dumps(res[-1]), flush=True)
         os.environ.pop("SFB_UNIFORM_VARIANT")
-        for kind, v in (("exponential", 0), ("exponential", 0x30), ("exponential", 0x40),
-                        ("exponential", 0x4000), ("uniform-integer", 0)):
+        for kind, v in (("exponential", 0), ("exponential", 0x10), ("exponential", 0x30),
+                        ("exponential", 0xa0), ("exponential", 0x4000), ("uniform-integer", 0)):
             os.environ["SFB_UNIFORM_VARIANT"] = str(v)
             out2 = out.view(torch.int64) if kind == "uniform-integer" else out
 
@@ -88,7 +88,15 @@ def main():
                         "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
             print(json.dumps(res[-1]), flush=True)
         os.environ.pop("SFB_UNIFORM_VARIANT", None)
-        os.environ.pop("SFB_UNIFORM_VARIANT", None)
+
+        def fn3():
+            launch_fill("exponential", cur, st.count, out, 65536, 65536, 65536, 1024, 1024,
+                        rate=0.37)
+
+        ms = timeit(fn3)
+        res.append({"w": "exponential_rate0.37_C5", "ms": ms,
+                    "gbs": out.numel() * 8 / (ms / 1e3) / 1e9})
+        print(json.dumps(res[-1]), flush=True)
         del out
         torch.cuda.empty_cache()
     if "vector" in what:  # the API's default use: a 1 x n vector on the default 64 x 8 grid
