@@ -692,7 +692,8 @@ def main():
                                        ms_per_step=ex["ms_per_step"],
                                        gbs=ex["alg_bytes"] / (ex["launch_ms"] / 1e3) / 1e9,
                                        config="SURVEY 8(f) item 1: fill_exponential (rate 1) on "
-                                              "the C5 layout, bit-exact glibc log1p port")
+                                              "the C5 layout, bit-exact glibc log1p port",
+                                       ncu_pipes=ncu_pipes("pipes_exponential"))
     if args.only is None and rank == 0:
         # the API's default use (configs[0]/C1 pattern at GPU scale): a 1 x n
         # vector on the default 64 x 8 grid, i.e. 8 active streams of 512

@@ -19,9 +19,9 @@ if [ -z "$NO_NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
       --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 4 --warmup 3 --no-cpu \
       > gpurun_out/ncu_bench_stdout.txt 2>&1
-  for K in ${KERNELS:-uniform normal fisher4 fisher10}; do
+  for K in ${KERNELS:-uniform exponential normal fisher4 fisher10}; do
     case $K in
-      uniform) RX="fill_uniform_";;
+      uniform|exponential) RX="fill_uniform_";;
       normal) RX="fill_normal_fast";;
       fisher4|fisher10) RX="fisher_kernel";;
     esac

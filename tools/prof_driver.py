@@ -1,7 +1,7 @@
 """Small driver for ncu captures: each hot kernel launched a few times at a
 size whose working set ncu can save/restore for kernel replay.
 
-    python tools/prof_driver.py [uniform|normal|fisher4|fisher10|all]
+    python tools/prof_driver.py [uniform|exponential|normal|fisher4|fisher10|all]
 """
 
 import os
@@ -27,13 +27,13 @@ def t10():
         return np.array(json.load(fh)["T10"])
 
 
-def uniform(reps=3):
+def uniform(reps=3, kind="uniform"):
     # C5 rows [0, 4096): 4096 x 65536 f64 = 2.1 GB, grid (1024, 1024), 2^20 streams
     st = sf.create_streams(sf.set_base_creator(), 1 << 20)[0]
     cur = st.device_current()
     out = torch.empty((4096, 65536), dtype=torch.float64, device="cuda")
     for _ in range(reps):
-        launch_fill("uniform", cur, st.count, out, 4096, 65536, 65536, 1024, 1024)
+        launch_fill(kind, cur, st.count, out, 4096, 65536, 65536, 1024, 1024)
     torch.cuda.synchronize()
 
 
@@ -61,6 +61,8 @@ def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("uniform", "all"):
         uniform()
+    if what in ("exponential", "all"):
+        uniform(kind="exponential")
     if what in ("normal", "all"):
         normal()
     if what in ("fisher4", "all"):

@@ -126,7 +126,7 @@ def main():
     # pipe utilisation of the compute-bound kernels (bench.py reports it beside
     # the algorithmic roofline)
     for rep in args:
-        for key in ("fisher4", "fisher10", "normal"):
+        for key in ("fisher4", "fisher10", "normal", "exponential"):
             if f"prof_{key}_" in os.path.basename(rep):
                 raw = ncu_csv(rep, "raw")
                 m = dict(zip(raw[0], raw[2]))
