@@ -391,3 +391,29 @@ class TestGrfFrontends:
                                       "grid": {"ncell_x": 2, "ncell_y": 2, "cell_size": 1.0},
                                       "streams": payload(4), "work_grid": [2, 2]})
         assert r.status_code == 422
+
+
+def test_fisher_plan_cache_keeps_validation_order():
+    """plan_fisher caches the host preparation per (table, n, grid); a cache
+    hit returns the same plan, still checks the stream count, and invalid
+    inputs raise the reference's errors in its order (table, n, streams --
+    fisher.py:134-139) whether or not a plan is cached."""
+    from paper_2201_06604_b200.errors import (InsufficientStreamsError, InvalidArgumentError)
+    from paper_2201_06604_b200.fisher import plan_fisher
+
+    t = [[3, 1], [1, 3]]
+    g = sf.WorkGrid(4, 2)
+    st = sf.StreamSet(np.ones((8, 6), np.int64), np.ones((8, 6), np.int64))
+    small = sf.StreamSet(np.ones((4, 6), np.int64), np.ones((4, 6), np.int64))
+    p1 = plan_fisher(t, 100, st, g)
+    assert plan_fisher(np.array(t), 100, st, g) is p1
+    assert plan_fisher(t, 101, st, g) is not p1
+    assert p1.sim_num == 104 and p1.reps == 13
+    with pytest.raises(InsufficientStreamsError):
+        plan_fisher(t, 100, small, g)          # cache hit: streams still checked
+    with pytest.raises(InvalidArgumentError):
+        plan_fisher(t, 0, small, g)            # n before streams
+    with pytest.raises(InvalidArgumentError):
+        plan_fisher([[-1, 2], [1, 1]], 0, small, g)  # table first
+    with pytest.raises(InvalidArgumentError):
+        plan_fisher([[-1, 2], [1, 1]], 100, st, g)   # never cached

@@ -90,3 +90,23 @@ def e2e_breakdown(reps=20):
 
 if __name__ == "__main__":
     e2e_breakdown()
+
+
+def e2e_loop(reps=200):
+    """Mean wall time of the bench's Fisher e2e step (host-authoritative states)."""
+    grid = sf.WorkGrid(256, 64)
+    st = sf.create_streams(sf.set_base_creator(), grid.size)[0]
+    for _ in range(5):
+        _ = st.current
+        sf.fisher_sim(T4, 10 ** 6, st, grid=grid)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        _ = st.current
+        sf.fisher_sim(T4, 10 ** 6, st, grid=grid)
+    ms = (time.perf_counter() - t0) * 1e3 / reps
+    print(f"e2e step {ms:.3f} ms = {1015808 / ms * 1e3:.3e} tables/s")
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        plan_fisher(T4, 10 ** 6, st, grid)
+    print(f"plan_fisher {1e3 * (time.perf_counter() - t0) / reps:.4f} ms")
