@@ -613,3 +613,46 @@ def test_download_shard_matches_column_selection(shape, g1, jr):
     want = np.concatenate([full[r, [c for c in range(shape[1]) if jr[0] <= c % g1 < jr[1]]]
                            for r in range(shape[0])])
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "uniform-integer", "exponential"])
+def test_generic_kernel_beyond_2p31_cells(kind):
+    """The generic kernel (odd g1) on a 46341 x 46347 matrix (2.15e9 cells >
+    2^31: 64-bit offsets everywhere): 4096 sampled cells, the four corners and
+    the final states of all 15 items against the oracle's skip-ahead."""
+    import torch
+
+    from paper_2201_06604_b200.grid import launch_fill
+
+    nrow, ncol, g0, g1 = 46341, 46347, 3, 5
+    assert nrow * ncol > 2 ** 31
+    st = fresh(g0 * g1)
+    cur = st.device_current()
+    dt = torch.int64 if kind == "uniform-integer" else torch.float64
+    out = torch.empty((nrow, ncol), dtype=dt, device="cuda")
+    launch_fill(kind, cur, st.count, out, nrow, ncol, ncol, g0, g1, rate=0.37)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(31)
+    rows = np.concatenate([rng.integers(0, nrow, 4096), [0, 0, nrow - 1, nrow - 1]])
+    cols = np.concatenate([rng.integers(0, ncol, 4096), [0, ncol - 1, 0, ncol - 1]])
+    got = out[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()].cpu().numpy()
+    seeds = oa.fresh_states(g0 * g1)
+    for r, c, v in zip(rows, cols, got):
+        i, j = r % g0, c % g1
+        w = i + g0 * j
+        ncols_item = (ncol - j + g1 - 1) // g1
+        s = orc.skip(seeds[w], (r // g0) * ncols_item + c // g1)
+        z = orc.step(s)
+        if kind == "uniform-integer":
+            want = z
+        elif kind == "uniform":
+            want = z * 2.0 ** -31
+        else:
+            want = -math.log1p(-(z * 2.0 ** -31)) / 0.37
+        assert v == want, (kind, r, c, v, want)
+    final = cur.cpu().numpy()
+    for w in rng.choice(g0 * g1, 15, replace=False):
+        i, j = w % g0, w // g0
+        nr_item = (nrow - i + g0 - 1) // g0
+        nc_item = (ncol - j + g1 - 1) // g1
+        assert np.array_equal(final[w], orc.skip(seeds[w], nr_item * nc_item)), w
