@@ -656,3 +656,48 @@ def test_generic_kernel_beyond_2p31_cells(kind):
         nr_item = (nrow - i + g0 - 1) // g0
         nc_item = (ncol - j + g1 - 1) // g1
         assert np.array_equal(final[w], orc.skip(seeds[w], nr_item * nc_item)), w
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_normal_beyond_2p31_cells(dtype):
+    """Box-Muller fill of a 46341 x 46345 matrix (> 2^31 cells; odd ncol, so
+    the last column's partner lane is discarded) on grid (3, 6): 4096 sampled
+    cells and the corners against the oracle's transform of skip-ahead draws
+    (float32: <= 1 ulp of float32(ref); float64: the 4-ulp contract)."""
+    import torch
+
+    from paper_2201_06604_b200.grid import launch_fill
+
+    nrow, ncol, g0, g1 = 46341, 46345, 3, 6
+    assert nrow * ncol > 2 ** 31
+    st = fresh(g0 * g1)
+    cur = st.device_current()
+    out = torch.empty((nrow, ncol), dtype=getattr(torch, dtype), device="cuda")
+    launch_fill("normal", cur, st.count, out, nrow, ncol, ncol, g0, g1)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(32)
+    rows = np.concatenate([rng.integers(0, nrow, 4096), [0, 0, nrow - 1, nrow - 1]])
+    cols = np.concatenate([rng.integers(0, ncol, 4096), [0, ncol - 1, 0, ncol - 1]])
+    got = out[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()].cpu().numpy()
+    seeds = oa.fresh_states(g0 * g1)
+    z1s, z2s = [], []
+    for r, c in zip(rows, cols):
+        i, j = r % g0, c % g1
+        j0 = j - (j & 1)
+        s0 = i * g1 + j0
+        idx = (r // g0) * ((ncol - j0 + g1 - 1) // g1) + c // g1
+        z1s.append(orc.step(orc.skip(seeds[s0], idx)))
+        z2s.append(orc.step(orc.skip(seeds[s0 + 1], idx)))
+    a, b = orc.box_muller(np.array(z1s), np.array(z2s))
+    want = np.where(cols % 2 == 0, a, b)
+    if dtype == "float32":
+        ref = want.astype(np.float32)
+        assert (np.abs(got.astype(np.float64) - ref) <= np.spacing(np.abs(ref))).all()
+    else:
+        assert_normal_f64_close(got, want)
+    final = cur.cpu().numpy()
+    for w in range(g0 * g1):
+        i, j = w // g1, w % g1
+        j0 = j - (j & 1)
+        n = ((nrow - i + g0 - 1) // g0) * ((ncol - j0 + g1 - 1) // g1)
+        assert np.array_equal(final[w], orc.skip(seeds[w], n)), w
