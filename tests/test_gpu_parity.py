@@ -701,3 +701,19 @@ def test_normal_beyond_2p31_cells(dtype):
         j0 = j - (j & 1)
         n = ((nrow - i + g0 - 1) // g0) * ((ncol - j0 + g1 - 1) // g1)
         assert np.array_equal(final[w], orc.skip(seeds[w], n)), w
+
+
+@pytest.mark.parametrize("table", [[[500000, 500000], [400000, 600000]],
+                                   [[300000, 2, 250000], [1, 310000, 5], [120000, 7, 20000]]])
+def test_fisher_large_totals(table):
+    """Totals in the millions (lf tables of ~8 MB in global memory, walks of
+    hundreds to thousands of steps, memo sets over +-7 sigma windows of
+    thousands of configurations): counts, statistics and states bit-exact."""
+    t = np.array(table)
+    st = fresh(64)
+    r = sf.fisher_sim(t, 3000, st, grid=grid((8, 8)), return_stats=True)
+    ref_st = oa.fresh_states(64)
+    ref = oa.fisher(t, 3000, ref_st, (8, 8), return_stats=True)
+    assert r.counts == ref["counts"] and r.sim_num == ref["sim_num"]
+    assert np.array_equal(r.statistics, ref["statistics"])
+    assert np.array_equal(st.current, ref_st)
