@@ -170,17 +170,30 @@ __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict_
     const int64_t d1 = min(d0 + m.chunk, total);
     Mrg s = load_state(cur + 6 * w);
     skip(tab, s, (uint64_t)d0);
+    // row segments of the item's draws: inside a segment the cells are g1
+    // apart, so the inner loop is a pointer bump (no per-cell index math)
     int64_t rho = d0 / nc, q = d0 % nc;
-    for (int64_t d = d0; d < d1; ++d) {
-        const uint32_t zm1 = step_m1(s);
+    for (int64_t d = d0; d < d1; ++rho, q = 0) {
+        const int64_t len = min(nc - q, d1 - d);
+        d += len;
         const int64_t off = (i + g.g0 * rho) * g.npad + j + g.g1 * q;
-        if (KIND == kInteger)
-            __stcs((long long *)out + off, (long long)zm1 + 1);
-        else
-            __stcs((double *)out + off, real_value<KIND>(zm1, rate));
-        if (++q == nc) {
-            q = 0;
-            ++rho;
+        if (KIND == kInteger) {
+            long long *p = (long long *)out + off;
+#pragma unroll 4
+            for (int64_t t = 0; t < len; ++t, p += g.g1) __stcs(p, (long long)step_m1(s) + 1);
+        } else {
+            double *p = (double *)out + off;
+            int64_t t = 0;
+            for (; t + 4 <= len; t += 4, p += 4 * g.g1) {  // 4 evaluations per basic block
+                uint32_t z[4];
+                double v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) z[k] = step_m1(s);
+                real_values<KIND, 4>(z, rate, v);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) __stcs(p + k * g.g1, v[k]);
+            }
+            for (; t < len; ++t, p += g.g1) __stcs(p, real_value<KIND>(step_m1(s), rate));
         }
     }
     if (d1 == total) store_state(cur + 6 * w, s);
@@ -456,19 +469,21 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
     Mrg sa = load_state(cur + 6 * s0), sb = load_state(cur + 6 * (s0 + 1));
     skip(tab, sa, (uint64_t)d0);
     skip(tab, sb, (uint64_t)d0);
+    // the partner lane of the row's last trip may lie past ncol (discarded,
+    // both streams still advance); row segments with a pointer bump inside
+    const int64_t q_nopartner = (j0 + g.g1 * (niter - 1) + 1 < g.ncol) ? -1 : niter - 1;
     int64_t rho = d0 / niter, q = d0 % niter;
-    for (int64_t d = d0; d < d1; ++d) {
-        T a, b;
-        const uint32_t z1 = step_m1(sa);
-        const uint32_t z2 = step_m1(sb);
-        bm<FAST>(z1, z2, bv, a, b);
-        const int64_t ca = j0 + g.g1 * q;
-        const int64_t off = (i + g.g0 * rho) * g.npad + ca;
-        __stcs(out + off, a);
-        if (ca + 1 < g.ncol) __stcs(out + off + 1, b);  // partner discarded past ncol
-        if (++q == niter) {
-            q = 0;
-            ++rho;
+    for (int64_t d = d0; d < d1; ++rho, q = 0) {
+        const int64_t len = min(niter - q, d1 - d);
+        d += len;
+        T *o = out + (i + g.g0 * rho) * g.npad + j0 + g.g1 * q;
+        for (int64_t t = 0; t < len; ++t, ++q, o += g.g1) {
+            T a, b;
+            const uint32_t z1 = step_m1(sa);
+            const uint32_t z2 = step_m1(sb);
+            bm<FAST>(z1, z2, bv, a, b);
+            __stcs(o, a);
+            if (q != q_nopartner) __stcs(o + 1, b);  // _kernels.py:151
         }
     }
     if (d1 == total) {
@@ -736,7 +751,8 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
     m.J = std::min(jeff, (item_hi - 1) / g.g0 + 1) - m.jlo;
     if (m.J <= 0) return SFB_OK;
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
-    m.chunk = std::max(kMinChunkDraws, ceil_div(maxdraws * ieff * m.J, kTargetUnits));
+    m.chunk = std::max<int64_t>(tune_knob("SFB_GENERIC_CHUNK", (int)kMinChunkDraws),
+                                ceil_div(maxdraws * ieff * m.J, kTargetUnits));
     m.chunk = std::min(m.chunk, std::max<int64_t>(1, maxdraws));
     m.nchunks = ceil_div(maxdraws, m.chunk);
     m.nunits = ieff * m.J * m.nchunks;
