@@ -442,8 +442,9 @@ __device__ __forceinline__ void bmN(const uint32_t *z1, const uint32_t *z2, cons
     }
 }
 
-// normal, generic layout: unit = (pair, chunk of pair-iterations)
-template <typename T, bool FAST>
+// normal, generic layout: unit = (pair, chunk of pair-iterations); PAIRED:
+// npad even and out 2-element aligned, so a lane pair is one 8/16-byte store
+template <typename T, bool FAST, bool PAIRED>
 __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__ cur,
                                                            T *__restrict__ out, Geom g, GenMap m,
                                                            const __grid_constant__ Pow2Table tab) {
@@ -477,13 +478,31 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
         const int64_t len = min(niter - q, d1 - d);
         d += len;
         T *o = out + (i + g.g0 * rho) * g.npad + j0 + g.g1 * q;
-        for (int64_t t = 0; t < len; ++t, ++q, o += g.g1) {
+        int64_t t = 0;
+        if (PAIRED) {  // three pairs per basic block (as the fast kernel)
+            const int64_t nfull = (q_nopartner >= 0 ? q_nopartner : niter) - q;
+            for (; t + 3 <= min(len, nfull); t += 3, q += 3, o += 3 * g.g1) {
+                uint32_t x[3], y[3];
+                step3(sa, x[0], x[1], x[2]);
+                step3(sb, y[0], y[1], y[2]);
+                T a[3], b[3];
+                bmN<FAST, 3>(x, y, bv, a, b);
+                put2(o, a[0], b[0]);
+                put2(o + g.g1, a[1], b[1]);
+                put2(o + 2 * g.g1, a[2], b[2]);
+            }
+        }
+        for (; t < len; ++t, ++q, o += g.g1) {
             T a, b;
             const uint32_t z1 = step_m1(sa);
             const uint32_t z2 = step_m1(sb);
             bm<FAST>(z1, z2, bv, a, b);
-            __stcs(o, a);
-            if (q != q_nopartner) __stcs(o + 1, b);  // _kernels.py:151
+            if (PAIRED && q != q_nopartner) {
+                put2(o, a, b);
+            } else {
+                __stcs(o, a);
+                if (q != q_nopartner) __stcs(o + 1, b);  // _kernels.py:151
+            }
         }
     }
     if (d1 == total) {
@@ -848,17 +867,20 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
     }
     if (m.J <= 0) return SFB_OK;
     const int64_t maxdraws = ceil_div(g.nrow, g.g0) * ceil_div(g.ncol, g.g1);
-    m.chunk = std::max(kMinChunkDraws,
-                       ceil_div(maxdraws * (i_end - m.i_lo) * m.J, kTargetUnits));
+    m.chunk = std::max<int64_t>(tune_knob("SFB_GENERIC_CHUNK", (int)kMinChunkDraws),
+                                ceil_div(maxdraws * (i_end - m.i_lo) * m.J, kTargetUnits));
     m.chunk = std::min(m.chunk, std::max<int64_t>(1, maxdraws));
     m.nchunks = ceil_div(maxdraws, m.chunk);
     m.nunits = (i_end - m.i_lo) * m.J * m.nchunks;
-    if (tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>()) & 4)
-        fill_normal_generic<T, false><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0,
-                                         st>>>(cur, out, g, m, tab);
+    const bool paired = g.npad % 2 == 0 && ((uintptr_t)out % (2 * sizeof(T))) == 0;
+    const unsigned nb = (unsigned)ceil_div(m.nunits, kThreads);
+    const bool exact = tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>()) & 4;
+    if (exact)
+        paired ? fill_normal_generic<T, false, true><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab)
+               : fill_normal_generic<T, false, false><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab);
     else
-        fill_normal_generic<T, true><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0,
-                                        st>>>(cur, out, g, m, tab);
+        paired ? fill_normal_generic<T, true, true><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab)
+               : fill_normal_generic<T, true, false><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab);
     return launch_check("fill_normal_generic");
 }
 

@@ -19,14 +19,16 @@ for ch in (512, 128, 256, 1024, 2048, 4096, 16384, 512):
     os.environ["SFB_GENERIC_CHUNK"] = str(ch)
     ms = timeit(lambda: launch_fill("uniform", cur, st.count, out, 1, n, n, 64, 8))
     print(json.dumps({"chunk": ch, "ms": round(ms, 4), "TBs": round(n*8/ms/1e9, 3)}), flush=True)
-os.environ.pop("SFB_GENERIC_CHUNK")
 for kind, dt in (("normal", torch.float64), ("normal", torch.float32), ("exponential", torch.float64),
                  ("uniform-integer", torch.int64)):
     o2 = torch.empty((1, n), dtype=dt, device="cuda")
-    ms = timeit(lambda: launch_fill(kind, cur, st.count, o2, 1, n, n, 64, 8))
-    print(json.dumps({"vector": kind, "dtype": str(dt), "ms": round(ms, 4),
-                      "TBs": round(n * o2.element_size() / ms / 1e9, 3)}), flush=True)
+    for ch in (512, 128, 256, 1024):
+        os.environ["SFB_GENERIC_CHUNK"] = str(ch)
+        ms = timeit(lambda: launch_fill(kind, cur, st.count, o2, 1, n, n, 64, 8))
+        print(json.dumps({"vector": kind, "dtype": str(dt), "chunk": ch, "ms": round(ms, 4),
+                          "TBs": round(n * o2.element_size() / ms / 1e9, 3)}), flush=True)
     del o2
+os.environ.pop("SFB_GENERIC_CHUNK")
 probe = torch.empty(n * 8, dtype=torch.uint8, device="cuda")
 from paper_2201_06604_b200 import _lib
 for v in (0, 1, 2):
