@@ -458,14 +458,22 @@ def reference_arm(args, rank, world):
                                        + ", all host cores"},
             "e2e": {"value": v, "unit": "uniforms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    # the unmodified reference's own numbers where it is installed, the
+    # oracle port's otherwise (both recorded)
+    nr = numba_reference(rows)
+    line["numba_reference"] = nr
     try:
-        line["workloads"] = {
-            "fisher_T4_tables_per_s": cpu_fisher(T4, 16384, 4),
-            "fisher_T10_tables_per_s": cpu_fisher(np.array(_t10()), 16384, 1),
-        }
+        port = {"fisher_T4_tables_per_s": cpu_fisher(T4, 16384, 4),
+                "fisher_T10_tables_per_s": cpu_fisher(np.array(_t10()), 16384, 1)}
     except Exception as e:  # noqa: BLE001
-        line["workloads"] = {"error": str(e)}
-    line["numba_reference"] = numba_reference(rows)
+        port = {"error": str(e)}
+    line["workloads"] = {k: nr.get(k, port.get(k)) for k in
+                         ("fisher_T4_tables_per_s", "fisher_T10_tables_per_s")}
+    if "fill_normal_per_s" in nr:
+        line["workloads"]["rnormGpu_f64_sample_per_s"] = nr["fill_normal_per_s"]
+    line["workloads"]["source"] = ("unmodified reference (baseline/_ref numba _kernels)"
+                                   if "fisher_T4_tables_per_s" in nr else "oracle port")
+    line["oracle_port"] = port
     try:
         if _import_reference() is None:
             raise RuntimeError("baseline/_ref not installed")
@@ -557,6 +565,28 @@ def numba_reference(rows):
         t0 = time.perf_counter()
         K.fisher_replicates(st16.copy(), t.sum(1), t.sum(0), lf, thr, 62, 16384, stats, False)
         res["fisher_T4_tables_per_s"] = 62 * 16384 / (time.perf_counter() - t0)
+        t = np.array(_t10())
+        lf = gammaln(np.arange(t.sum() + 1, dtype=np.float64) + 1.0)
+        thr = float(-gammaln(t + 1.0).sum())
+        thr += 1e-7 * abs(thr)
+        t0 = time.perf_counter()
+        K.fisher_replicates(st16.copy(), t.sum(1), t.sum(0), lf, thr, 8, 16384, stats, False)
+        res["fisher_T10_tables_per_s"] = 8 * 16384 / (time.perf_counter() - t0)
+        # configs[1] layout (2^18 streams on grid (512,512), 32000 columns),
+        # rows [0, 1024): 3.3e7 float64 normals (the reference has no float32)
+        st18, _ = orc.create_streams((12345,) * 6, 1 << 18)
+        nout = np.zeros((1024, 32000))
+        K.fill_normal(st18.copy(), nout.ravel(), 16, 32000, 32000, 512, 512)  # JIT warm-up
+        best = None
+        for _ in range(3):
+            cur = st18.copy()
+            t0 = time.perf_counter()
+            K.fill_normal(cur, nout.ravel(), 1024, 32000, 32000, 512, 512)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        res["fill_normal_per_s"] = 1024 * 32000 / best
+        res["fill_normal_sample"] = ("configs[1] layout rows [0,1024) via _kernels.fill_normal "
+                                     "(float64), best of 3")
         return res
     except Exception as e:  # noqa: BLE001
         return {"unavailable": f"{type(e).__name__}: {e}"}
