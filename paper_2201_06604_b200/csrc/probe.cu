@@ -68,13 +68,44 @@ __global__ void __launch_bounds__(256) write_probe_seg256_kernel(double *out, in
                      : "memory");
 }
 
+// TMA bulk-store probe: every warp's lane 0 streams its CTA's contiguous
+// segment out of one shared-memory chunk with cp.async.bulk (no registers in
+// the data path); chunks of kBulkChunk bytes interleaved across the 8 warps
+constexpr int kBulkChunk = 16384;
+__global__ void __launch_bounds__(256) write_probe_bulk_kernel(unsigned char *out, int64_t bytes,
+                                                               int64_t seg) {
+    __shared__ __align__(128) unsigned char buf[kBulkChunk];
+    for (int i = threadIdx.x; i < kBulkChunk / 8; i += 256) ((double *)buf)[i] = 1.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const int64_t b0 = (int64_t)blockIdx.x * seg, b1 = min(b0 + seg, bytes);
+    if ((threadIdx.x & 31) == 0) {
+        const int w = threadIdx.x >> 5;
+        const uint32_t src = (uint32_t)__cvta_generic_to_shared(buf);
+        for (int64_t off = b0 + (int64_t)w * kBulkChunk; off < b1; off += 8LL * kBulkChunk) {
+            const uint32_t n = (uint32_t)min((int64_t)kBulkChunk, b1 - off);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(out + off), "r"(src), "r"(n) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
 }  // namespace sfb
 
 using namespace sfb;
 
 extern "C" int sfb_probe_write(void *d_out, int64_t bytes, int variant, void *stream) {
     const int64_t n = bytes / 16;
-    if (variant == 2) {
+    if (variant == 3 || variant == 4) {  // TMA bulk stores; 4: 2 CTAs per SM
+        const int64_t blocks = 148 * (variant == 3 ? 8 : 2);
+        const int64_t seg = ((bytes + blocks - 1) / blocks + kBulkChunk - 1) / kBulkChunk *
+                            kBulkChunk;
+        write_probe_bulk_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+            (unsigned char *)d_out, bytes, seg);
+    } else if (variant == 2) {
         const int64_t n4 = bytes / 32;
         const int64_t blocks = 148 * 64;
         const int64_t seg = (n4 + blocks - 1) / blocks;
