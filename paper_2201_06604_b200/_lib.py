@@ -10,6 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -117,6 +119,28 @@ def ptr(a, t=_i64p):
 def dptr(t) -> int:
     """raw device address of a torch tensor."""
     return t.data_ptr()
+
+
+# device -> numpy through a pinned block of torch's caching host allocator:
+# one DMA at PCIe speed (a fresh pageable .cpu() runs at ~2 GB/s: page faults
+# plus a staged copy; 800 MB: 400 ms vs 15 ms once the block is cached).
+# Above this size the array stays pageable (pinned blocks stay cached).
+PINNED_HOST_MAX = 4 << 30
+
+
+def to_host(t) -> np.ndarray:
+    """numpy copy of a CUDA tensor (synchronous)."""
+    import torch
+
+    nbytes = t.numel() * t.element_size()
+    if t.is_cuda and 0 < nbytes <= PINNED_HOST_MAX:
+        try:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        except RuntimeError:
+            return t.cpu().numpy()
+        h.copy_(t)
+        return h.numpy()
+    return t.cpu().numpy()
 
 
 _DEVICE_OK = False

@@ -93,7 +93,7 @@ class MatrixBuffer:
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            self._host = self.tensor.cpu().numpy()
+            self._host = _lib.to_host(self.tensor)
         return self._host
 
     @property

@@ -34,7 +34,12 @@ def _dev(a):
 
 
 def _back(host, dev):
-    host[...] = dev.cpu().numpy().reshape(host.shape)
+    import torch
+
+    if host.flags.c_contiguous and host.size == dev.numel():
+        torch.from_numpy(host).view(dev.dtype).reshape(dev.shape).copy_(dev)  # one copy
+    else:
+        host[...] = dev.cpu().numpy().reshape(host.shape)
 
 
 def max_threads():  # _kernels.py:25-26
@@ -94,7 +99,7 @@ def fisher_replicates(cur, nrowt, ncolt, lf, threshold, reps, nitems, stats,
         _lib.stream_handle()))
     _back(cur, dcur)
     if want_stats:
-        stats[: nitems * reps] = dstats[: nitems * reps].cpu().numpy()
+        _back(stats[: nitems * reps], dstats[: nitems * reps])
     return int(count.item())
 
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _lib
 from .errors import InvalidArgumentError
 from .fisher import FisherResult, launch_fisher, plan_fisher
 from .grid import KIND_DTYPES, MatrixBuffer, _check_streams, launch_fill
@@ -64,8 +65,6 @@ class DeviceExecutor:
 
     def __init__(self):
         import torch
-
-        from . import _lib
 
         _lib.require_device()
         self.device = torch.device("cuda", torch.cuda.current_device())
@@ -147,7 +146,7 @@ def fisher_sim_sharded(table, n, streams, grid, return_stats=False, group=None,
                 a, b = shard_range(plan.nitems, r, world)
                 pieces.append(part[: (b - a) * plan.reps])
             stats = torch.cat(pieces)
-        full_stats = stats.cpu().numpy()
+        full_stats = _lib.to_host(stats)
     if world > 1:
         _allgather_rows(executor, streams, lo, hi, group)
     return FisherResult(threshold=plan.threshold, sim_num=plan.sim_num, counts=counts,
