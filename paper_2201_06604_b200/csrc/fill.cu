@@ -29,6 +29,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "box_muller.cuh"
 #include "log1p_glibc.cuh"
@@ -151,7 +152,7 @@ struct GenMap {
 
 // uniform kinds, generic layout
 template <int KIND>
-__global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict__ cur,
+__global__ void __launch_bounds__(256) fill_uniform_generic(StateIO io,
                                                             void *__restrict__ out, Geom g,
                                                             GenMap m, RateArg rate,
                                                             const __grid_constant__ Pow2Table tab) {
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict_
     const int64_t d0 = c * m.chunk;
     if (d0 >= total) return;
     const int64_t d1 = min(d0 + m.chunk, total);
-    Mrg s = load_state(cur + 6 * w);
+    Mrg s = load_state(io, w);
     skip(tab, s, (uint64_t)d0);
     // row segments of the item's draws: inside a segment the cells are g1
     // apart, so the inner loop is a pointer bump (no per-cell index math)
@@ -196,13 +197,13 @@ __global__ void __launch_bounds__(256) fill_uniform_generic(int64_t *__restrict_
             for (; t < len; ++t, p += g.g1) __stcs(p, real_value<KIND>(step_m1(s), rate));
         }
     }
-    if (d1 == total) store_state(cur + 6 * w, s);
+    if (d1 == total) store_state(io, w, s);
 }
 
 // uniform kinds, column-pair fast path (g1 even, npad even, shard = whole pairs)
 // unit = (chunk c, grid row i, pair jp): adjacent lanes = adjacent pairs
 template <int KIND, int MINB, int NT = 256>
-__global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(int64_t *__restrict__ cur,
+__global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(StateIO io,
                                                          void *__restrict__ out, Geom g,
                                                          int64_t j_lo, int64_t npairs,
                                                          int64_t rows_per_chunk, int64_t nunits,
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(int64_t *__restric
     const int64_t rho1 = min(rho0 + rows_per_chunk, nr);
     const int64_t na = owned(g.ncol, j, g.g1), nb = owned(g.ncol, j + 1, g.g1);
     const int64_t wa = i + g.g0 * j, wb = wa + g.g0;
-    Mrg sa = load_state(cur + 6 * wa), sb = load_state(cur + 6 * wb);
+    Mrg sa = load_state(io, wa), sb = load_state(io, wb);
     if (rho0) {
         skip(tab, sa, (uint64_t)(rho0 * na));
         skip(tab, sb, (uint64_t)(rho0 * nb));
@@ -242,8 +243,8 @@ __global__ void __launch_bounds__(NT, MINB) fill_uniform_fast(int64_t *__restric
         if (na > nb) put_one<KIND>(out, rowoff + g.g1 * nb, step_m1(sa), rate);
     }
     if (rho1 == nr) {
-        store_state(cur + 6 * wa, sa);
-        store_state(cur + 6 * wb, sb);
+        store_state(io, wa, sa);
+        store_state(io, wb, sb);
     }
 }
 
@@ -276,7 +277,7 @@ __device__ __forceinline__ void put_quad(void *out, int64_t off, uint32_t z0, ui
 }
 
 template <int KIND, int MINB, bool STEP3 = true>
-__global__ void __launch_bounds__(256, MINB) fill_uniform_quad(int64_t *__restrict__ cur,
+__global__ void __launch_bounds__(256, MINB) fill_uniform_quad(StateIO io,
                                                          void *__restrict__ out, Geom g,
                                                          int64_t j_lo, int64_t nquads,
                                                          int64_t rows_per_chunk, int64_t nunits,
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(256, MINB) fill_uniform_quad(int64_t *__restri
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         n[k] = owned(g.ncol, j + k, g.g1);  // nonincreasing in k, by at most one
-        s[k] = load_state(cur + 6 * (i + g.g0 * (j + k)));
+        s[k] = load_state(io, i + g.g0 * (j + k));
         if (rho0) skip(tab, s[k], (uint64_t)(rho0 * n[k]));
     }
     for (int64_t rho = rho0; rho < rho1; ++rho) {
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(256, MINB) fill_uniform_quad(int64_t *__restri
     }
     if (rho1 == nr) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) store_state(cur + 6 * (i + g.g0 * (j + k)), s[k]);
+        for (int k = 0; k < 4; ++k) store_state(io, i + g.g0 * (j + k), s[k]);
     }
 }
 
@@ -445,7 +446,7 @@ __device__ __forceinline__ void bmN(const uint32_t *z1, const uint32_t *z2, cons
 // normal, generic layout: unit = (pair, chunk of pair-iterations); PAIRED:
 // npad even and out 2-element aligned, so a lane pair is one 8/16-byte store
 template <typename T, bool FAST, bool PAIRED>
-__global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__ cur,
+__global__ void __launch_bounds__(256) fill_normal_generic(StateIO io,
                                                            T *__restrict__ out, Geom g, GenMap m,
                                                            const __grid_constant__ Pow2Table tab) {
     __shared__ __align__(16) unsigned char bm_raw[kBmSmemBytes];
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
     const int64_t d0 = c * m.chunk;
     if (d0 >= total) return;
     const int64_t d1 = min(d0 + m.chunk, total);
-    Mrg sa = load_state(cur + 6 * s0), sb = load_state(cur + 6 * (s0 + 1));
+    Mrg sa = load_state(io, s0), sb = load_state(io, s0 + 1);
     skip(tab, sa, (uint64_t)d0);
     skip(tab, sb, (uint64_t)d0);
     // the partner lane of the row's last trip may lie past ncol (discarded,
@@ -506,8 +507,8 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
         }
     }
     if (d1 == total) {
-        store_state(cur + 6 * s0, sa);
-        store_state(cur + 6 * (s0 + 1), sb);
+        store_state(io, s0, sa);
+        store_state(io, s0 + 1, sb);
     }
 }
 
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(256) fill_normal_generic(int64_t *__restrict__
 //               thread have the same trip count and always-valid partners; one
 //               16-byte store (float32) per trip.
 template <typename T, int PAIRS, int MINB, bool FAST>
-__global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restrict__ cur,
+__global__ void __launch_bounds__(256, MINB) fill_normal_fast(StateIO io,
                                                         T *__restrict__ out, Geom g,
                                                         int64_t i_lo, int64_t nrows_grid,
                                                         int64_t rows_per_chunk, int64_t nunits,
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
     Mrg st[2 * PAIRS];
 #pragma unroll
     for (int k = 0; k < 2 * PAIRS; ++k) {
-        st[k] = load_state(cur + 6 * (s0 + k));
+        st[k] = load_state(io, s0 + k);
         if (rho0) skip(tab, st[k], (uint64_t)(rho0 * niter));
     }
     if (PAIRS == 2) {
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(256, MINB) fill_normal_fast(int64_t *__restric
     }
     if (rho1 == nr) {
 #pragma unroll
-        for (int k = 0; k < 2 * PAIRS; ++k) store_state(cur + 6 * (s0 + k), st[k]);
+        for (int k = 0; k < 2 * PAIRS; ++k) store_state(io, s0 + k, st[k]);
     }
 }
 
@@ -648,6 +649,45 @@ static int zero_padding(void *out, size_t elsize, int64_t nrow, int64_t ncol, in
     cudaError_t e = cudaMemset2DAsync((char *)out + ncol * elsize, npad * elsize, 0,
                                       (npad - ncol) * elsize, nrow, st);
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "padding memset: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+StateSnapshot::~StateSnapshot() {
+    if (buf) cudaFreeAsync(buf, st);
+}
+
+int make_state_io(int64_t *cur, int64_t lo, int64_t hi, bool chunked, cudaStream_t st,
+                  StateSnapshot &snap, StateIO *io) {
+    io->out = cur;
+    io->in = cur;
+    io->in_lo = 0;
+    if (!chunked || hi <= lo) return SFB_OK;
+    // keep up to 1 GiB of freed snapshot memory in the device's default pool
+    // (otherwise it is returned to the driver at every synchronisation)
+    static std::atomic<uint64_t> pool_done{0};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!(pool_done.load() & (1ull << (d & 63)))) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+            uint64_t keep = 0;
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            if (keep < (1ull << 30)) {
+                keep = 1ull << 30;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
+        pool_done.fetch_or(1ull << (d & 63));
+    }
+    const size_t bytes = (size_t)(hi - lo) * 6 * sizeof(int64_t);
+    cudaError_t e = cudaMallocAsync((void **)&snap.buf, bytes, st);
+    if (e == cudaSuccess) {
+        snap.st = st;
+        e = cudaMemcpyAsync(snap.buf, cur + 6 * lo, bytes, cudaMemcpyDeviceToDevice, st);
+    }
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "state snapshot: %s", cudaGetErrorString(e));
+    io->in = snap.buf;
+    io->in_lo = lo;
     return SFB_OK;
 }
 
@@ -700,6 +740,10 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
             qchunks = ceil_div(rows, qrpc);
             const int64_t qunits = qbase * qchunks;
             const unsigned qb = (unsigned)ceil_div(qunits, kThreads);
+            StateSnapshot snap;
+            StateIO io;
+            if (int rc = make_state_io(cur, item_lo, item_hi, qchunks > 1, st, snap, &io))
+                return rc;
             // register cap / single-step variants (tuning); the exponential's
             // twelve log1p evaluations in flight want 3 CTAs/SM (measured 19.4 ->
             // 15.4 ms on C5), the store-bound kinds the uncapped default
@@ -707,53 +751,56 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
             if (sel == 0 && KIND == kExponential) sel = 3;
             switch (sel) {
                 case 3:
-                    fill_uniform_quad<KIND, 3><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
+                    fill_uniform_quad<KIND, 3><<<qb, kThreads, 0, st>>>(io, out, g, j_lo, nquads,
                                                                         qrpc, qunits, rate, tab);
                     break;
                 case 4:
-                    fill_uniform_quad<KIND, 4><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
+                    fill_uniform_quad<KIND, 4><<<qb, kThreads, 0, st>>>(io, out, g, j_lo, nquads,
                                                                         qrpc, qunits, rate, tab);
                     break;
                 case 9:
                     fill_uniform_quad<KIND, 1, false><<<qb, kThreads, 0, st>>>(
-                        cur, out, g, j_lo, nquads, qrpc, qunits, rate, tab);
+                        io, out, g, j_lo, nquads, qrpc, qunits, rate, tab);
                     break;
                 case 10:
                     fill_uniform_quad<KIND, 3, false><<<qb, kThreads, 0, st>>>(
-                        cur, out, g, j_lo, nquads, qrpc, qunits, rate, tab);
+                        io, out, g, j_lo, nquads, qrpc, qunits, rate, tab);
                     break;
                 default:
-                    fill_uniform_quad<KIND, 1><<<qb, kThreads, 0, st>>>(cur, out, g, j_lo, nquads,
+                    fill_uniform_quad<KIND, 1><<<qb, kThreads, 0, st>>>(io, out, g, j_lo, nquads,
                                                                         qrpc, qunits, rate, tab);
             }
             return launch_check("fill_uniform_quad");
         }
+        StateSnapshot snap;
+        StateIO io;
+        if (int rc = make_state_io(cur, item_lo, item_hi, nchunks > 1, st, snap, &io)) return rc;
         if ((v >> 12) & 3) {  // bits 12-13: 512 / 1024 threads per CTA
             const int nt = (v >> 12) == 1 ? 512 : 1024;
             const unsigned b2 = (unsigned)ceil_div(nunits, nt);
             if (nt == 512)
-                fill_uniform_fast<KIND, 1, 512><<<b2, 512, 0, st>>>(cur, out, g, j_lo, npairs, rpc,
+                fill_uniform_fast<KIND, 1, 512><<<b2, 512, 0, st>>>(io, out, g, j_lo, npairs, rpc,
                                                                    nunits, rate, tab);
             else
-                fill_uniform_fast<KIND, 1, 1024><<<b2, 1024, 0, st>>>(cur, out, g, j_lo, npairs,
+                fill_uniform_fast<KIND, 1, 1024><<<b2, 1024, 0, st>>>(io, out, g, j_lo, npairs,
                                                                      rpc, nunits, rate, tab);
             return launch_check("fill_uniform_fast");
         }
         switch ((v >> 4) & 15) {
             case 4:
-                fill_uniform_fast<KIND, 4><<<blocks, kThreads, 0, st>>>(cur, out, g, j_lo, npairs,
+                fill_uniform_fast<KIND, 4><<<blocks, kThreads, 0, st>>>(io, out, g, j_lo, npairs,
                                                                        rpc, nunits, rate, tab);
                 break;
             case 6:
-                fill_uniform_fast<KIND, 6><<<blocks, kThreads, 0, st>>>(cur, out, g, j_lo, npairs,
+                fill_uniform_fast<KIND, 6><<<blocks, kThreads, 0, st>>>(io, out, g, j_lo, npairs,
                                                                        rpc, nunits, rate, tab);
                 break;
             case 8:
-                fill_uniform_fast<KIND, 8><<<blocks, kThreads, 0, st>>>(cur, out, g, j_lo, npairs,
+                fill_uniform_fast<KIND, 8><<<blocks, kThreads, 0, st>>>(io, out, g, j_lo, npairs,
                                                                        rpc, nunits, rate, tab);
                 break;
             default:
-                fill_uniform_fast<KIND, 1><<<blocks, kThreads, dsmem, st>>>(cur, out, g, j_lo,
+                fill_uniform_fast<KIND, 1><<<blocks, kThreads, dsmem, st>>>(io, out, g, j_lo,
                                                                            npairs, rpc, nunits,
                                                                            rate, tab);
         }
@@ -775,8 +822,11 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
     m.chunk = std::min(m.chunk, std::max<int64_t>(1, maxdraws));
     m.nchunks = ceil_div(maxdraws, m.chunk);
     m.nunits = ieff * m.J * m.nchunks;
+    StateSnapshot snap;
+    StateIO io;
+    if (int rc = make_state_io(cur, item_lo, item_hi, m.nchunks > 1, st, snap, &io)) return rc;
     fill_uniform_generic<KIND><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0, st>>>(
-        cur, out, g, m, rate, tab);
+        io, out, g, m, rate, tab);
     return launch_check("fill_uniform_generic");
 }
 
@@ -785,32 +835,32 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
 // bit 2 -> float32 via the exact float64 transform instead of
 // box_muller_pair_f32
 template <typename T, int PAIRS, bool FAST>
-static void launch_normal_fast_minb(int minb, unsigned blocks, cudaStream_t st, int64_t *cur,
+static void launch_normal_fast_minb(int minb, unsigned blocks, cudaStream_t st, StateIO io,
                                     T *out, const Geom &g, int64_t i_lo, int64_t nrows_grid,
                                     int64_t rpc, int64_t nunits, const Pow2Table &tab) {
     if (minb >= 4)
-        fill_normal_fast<T, PAIRS, 4, FAST><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+        fill_normal_fast<T, PAIRS, 4, FAST><<<blocks, kThreads, 0, st>>>(io, out, g, i_lo,
                                                                          nrows_grid, rpc, nunits, tab);
     else if (minb == 3)
-        fill_normal_fast<T, PAIRS, 3, FAST><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+        fill_normal_fast<T, PAIRS, 3, FAST><<<blocks, kThreads, 0, st>>>(io, out, g, i_lo,
                                                                          nrows_grid, rpc, nunits, tab);
     else
-        fill_normal_fast<T, PAIRS, 1, FAST><<<blocks, kThreads, 0, st>>>(cur, out, g, i_lo,
+        fill_normal_fast<T, PAIRS, 1, FAST><<<blocks, kThreads, 0, st>>>(io, out, g, i_lo,
                                                                          nrows_grid, rpc, nunits, tab);
 }
 
 template <typename T, bool FAST>
-static void launch_normal_fast(bool two, int minb, cudaStream_t st, int64_t *cur, T *out,
+static void launch_normal_fast(bool two, int minb, cudaStream_t st, StateIO io, T *out,
                                const Geom &g, int64_t i_lo, int64_t nrows_grid, int64_t rpc,
                                int64_t nunits) {
     Pow2Table tab;
     pow2_table(&tab);
     const unsigned blocks = (unsigned)ceil_div(nunits, kThreads);
     if (two)
-        launch_normal_fast_minb<T, 2, FAST>(minb, blocks, st, cur, out, g, i_lo, nrows_grid, rpc,
+        launch_normal_fast_minb<T, 2, FAST>(minb, blocks, st, io, out, g, i_lo, nrows_grid, rpc,
                                             nunits, tab);
     else
-        launch_normal_fast_minb<T, 1, FAST>(minb, blocks, st, cur, out, g, i_lo, nrows_grid, rpc,
+        launch_normal_fast_minb<T, 1, FAST>(minb, blocks, st, io, out, g, i_lo, nrows_grid, rpc,
                                             nunits, tab);
 }
 
@@ -843,10 +893,13 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
         // one pair per thread where two would fit: twice the units
         const int64_t nu = (two && !use_two) ? nunits * 2 : nunits;
         const int minb = (v & 1) ? 4 : (v & 8) ? 3 : 1;
+        StateSnapshot snap;
+        StateIO io;
+        if (int rc = make_state_io(cur, item_lo, item_hi, nchunks > 1, st, snap, &io)) return rc;
         if (v & 4)
-            launch_normal_fast<T, false>(use_two, minb, st, cur, out, g, i_lo, nrows_grid, rpc, nu);
+            launch_normal_fast<T, false>(use_two, minb, st, io, out, g, i_lo, nrows_grid, rpc, nu);
         else
-            launch_normal_fast<T, true>(use_two, minb, st, cur, out, g, i_lo, nrows_grid, rpc, nu);
+            launch_normal_fast<T, true>(use_two, minb, st, io, out, g, i_lo, nrows_grid, rpc, nu);
         return launch_check("fill_normal_fast");
     }
     // pairs with owned cells: grid rows of the shard below min(g0, nrow),
@@ -874,13 +927,16 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
     m.nunits = (i_end - m.i_lo) * m.J * m.nchunks;
     const bool paired = g.npad % 2 == 0 && ((uintptr_t)out % (2 * sizeof(T))) == 0;
     const unsigned nb = (unsigned)ceil_div(m.nunits, kThreads);
+    StateSnapshot snap;
+    StateIO io;
+    if (int rc = make_state_io(cur, item_lo, item_hi, m.nchunks > 1, st, snap, &io)) return rc;
     const bool exact = tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>()) & 4;
     if (exact)
-        paired ? fill_normal_generic<T, false, true><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab)
-               : fill_normal_generic<T, false, false><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab);
+        paired ? fill_normal_generic<T, false, true><<<nb, kThreads, 0, st>>>(io, out, g, m, tab)
+               : fill_normal_generic<T, false, false><<<nb, kThreads, 0, st>>>(io, out, g, m, tab);
     else
-        paired ? fill_normal_generic<T, true, true><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab)
-               : fill_normal_generic<T, true, false><<<nb, kThreads, 0, st>>>(cur, out, g, m, tab);
+        paired ? fill_normal_generic<T, true, true><<<nb, kThreads, 0, st>>>(io, out, g, m, tab)
+               : fill_normal_generic<T, true, false><<<nb, kThreads, 0, st>>>(io, out, g, m, tab);
     return launch_check("fill_normal_generic");
 }
 

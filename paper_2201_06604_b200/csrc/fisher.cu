@@ -55,7 +55,9 @@ using ChunkJumps = ChunkJumpsN<kMaxChunks>;
 using ChunkJumpsLarge = ChunkJumpsN<kMaxChunksLarge>;
 
 struct FisherArgs {
-    int64_t *cur;
+    int64_t *cur;             // final states (the item's last chunk writes them)
+    const int64_t *cur_in;    // start states of streams cur_in_lo.. (a snapshot when chunked)
+    int64_t cur_in_lo;
     const int32_t *rowm;  // device margins (int32; totals < 2^31 checked)
     const int32_t *colm;
     const double *lf;
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         const int64_t rep0 = c * a.rpc;
         const int64_t rep1 = min(rep0 + a.rpc, a.reps);
         if (rep0 < rep1) {
-            Mrg s = load_state(a.cur + 6 * w);
+            Mrg s = load_state(a.cur_in + 6 * (w - a.cur_in_lo));
             if (c) apply(jumps.j[c], s);
             int *jw = jwork + threadIdx.x;
             const MemoSet *mp = a.use_memo ? &memo : nullptr;
@@ -277,9 +279,12 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
             c.dev_cap = std::max(bytes + 64, (size_t)1 << 20);  // +64: 16-byte block copies
             e = cudaMalloc((void **)&c.dev, c.dev_cap);
         }
-        if (e == cudaSuccess && bytes > c.pin_cap) {
+        // uploaded in whole 16-byte blocks (the kernel's memo staging copies
+        // uint4s), the tail zero-filled so no uninitialised byte is ever read
+        const size_t up = align16(bytes);
+        if (e == cudaSuccess && up > c.pin_cap) {
             if (c.pinned) cudaFreeHost(c.pinned);
-            c.pin_cap = std::max(bytes, (size_t)1 << 20);
+            c.pin_cap = std::max(up, (size_t)1 << 20);
             e = cudaMallocHost((void **)&c.pinned, c.pin_cap);
         }
         if (e == cudaSuccess) {
@@ -291,7 +296,8 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
                 memcpy(c.pinned + acc_off, hm->acc.data(), hm->acc.size() * 8);
                 memcpy(c.pinned + k_off, hm->k.data(), hm->k.size() * 4);
             }
-            e = cudaMemcpyAsync(c.dev, c.pinned, bytes, cudaMemcpyHostToDevice, st);
+            memset(c.pinned + bytes, 0, up - bytes);
+            e = cudaMemcpyAsync(c.dev, c.pinned, up, cudaMemcpyHostToDevice, st);
         }
         if (e == cudaSuccess && c.last_use == nullptr)
             e = cudaEventCreateWithFlags(&c.last_use, cudaEventDisableTiming);
@@ -465,11 +471,16 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     jump_pow(0, &jl.j[0]);
     for (int64_t c = 1; c < nchunks; ++c) jump_mul(jl.j[c - 1], step, &jl.j[c]);
     const bool large = nchunks > kMaxChunks;
+    StateSnapshot snap;
+    StateIO io;
+    if (int rc = make_state_io(d_cur, item_lo, item_hi, nchunks > 1, st, snap, &io)) return rc;
     ChunkJumps jumps;
     if (!large) memcpy(jumps.j, jl.j, sizeof(Jump) * (size_t)nchunks);
 
     FisherArgs a;
-    a.cur = d_cur;
+    a.cur = io.out;
+    a.cur_in = io.in;
+    a.cur_in_lo = io.in_lo;
     a.rowm = rowm;
     a.colm = colm;
     a.lf = lfd;
