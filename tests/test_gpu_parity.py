@@ -717,3 +717,37 @@ def test_fisher_large_totals(table):
     assert r.counts == ref["counts"] and r.sim_num == ref["sim_num"]
     assert np.array_equal(r.statistics, ref["statistics"])
     assert np.array_equal(st.current, ref_st)
+
+
+def test_concurrent_host_threads_match_serial(G):
+    """Four host threads calling fisher_sim (different tables: the per-device
+    input cache switches under its lock), fills and rcont2 concurrently give
+    the serial results."""
+    import threading
+
+    tables = [np.array(G["T4"]), np.array(G["T10"]), np.array([[3, 7], [6, 2]]),
+              np.array([[5, 0, 4], [2, 6, 1]])]
+
+    def work(t):
+        st = fresh(256)
+        r = sf.fisher_sim(t, 5000, st, grid=grid((16, 16)), return_stats=True)
+        st2 = fresh(64)
+        u = sf.fill_uniform(st2, sf.FillRequest(shape=(300, 200), grid=grid((8, 8)))).data
+        s6 = fresh(1).current[0].copy()
+        tab = sf.rcont2(t.sum(1), t.sum(0), s6)
+        return (r.counts, r.statistics.tobytes(), st.current.tobytes(), u.tobytes(),
+                st2.current.tobytes(), tab.tobytes(), s6.tobytes())
+
+    serial = [work(t) for t in tables]
+    for _ in range(3):
+        out = [None] * len(tables)
+
+        def run(i):
+            out[i] = work(tables[i])
+
+        th = [threading.Thread(target=run, args=(i,)) for i in range(len(tables))]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        assert out == serial
