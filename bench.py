@@ -138,6 +138,10 @@ class Timer:
 
     def stop(self):
         self.e.record()
+        # poll instead of a blocking synchronize: the sleeps release the GIL so
+        # the NVML clock sampler keeps sampling during the timed region
+        while not self.e.query():
+            time.sleep(0.0002)
         self.e.synchronize()
         return self.s.elapsed_time(self.e)  # ms
 

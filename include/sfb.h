@@ -19,10 +19,11 @@
  *   - stream states use the reference layout: int64 (n, 6) C-contiguous,
  *     row w = (g1[0..2], g2[0..2]) newest-first (core.py:161-172), mutated in
  *     place exactly where the reference kernels mutate `cur`;
- *   - a launch that splits a stream's draws over several threads first takes
- *     a stream-ordered snapshot of the launch's state rows (cudaMallocAsync on
- *     the device's default pool, 48 bytes per stream, freed after the kernel),
- *     so the result never depends on thread-block scheduling.
+ *   - results never depend on thread-block scheduling: a fill that splits a
+ *     stream's draws over several threads reads start states from a
+ *     stream-ordered snapshot of its state rows (cudaMallocAsync on the
+ *     device's default pool, 48 bytes per stream, freed after the kernel); a
+ *     chunked Fisher launch advances the states in a second kernel.
  */
 #ifndef SFB_H_
 #define SFB_H_

@@ -55,9 +55,8 @@ using ChunkJumps = ChunkJumpsN<kMaxChunks>;
 using ChunkJumpsLarge = ChunkJumpsN<kMaxChunksLarge>;
 
 struct FisherArgs {
-    int64_t *cur;             // final states (the item's last chunk writes them)
-    const int64_t *cur_in;    // start states of streams cur_in_lo.. (a snapshot when chunked)
-    int64_t cur_in_lo;
+    int64_t *cur;             // start states; final states too when store_final
+    int store_final;          // one thread per item: it writes its final state
     const int32_t *rowm;  // device margins (int32; totals < 2^31 checked)
     const int32_t *colm;
     const double *lf;
@@ -125,7 +124,7 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         const int64_t rep0 = c * a.rpc;
         const int64_t rep1 = min(rep0 + a.rpc, a.reps);
         if (rep0 < rep1) {
-            Mrg s = load_state(a.cur_in + 6 * (w - a.cur_in_lo));
+            Mrg s = load_state(a.cur + 6 * w);
             if (c) apply(jumps.j[c], s);
             int *jw = jwork + threadIdx.x;
             const MemoSet *mp = a.use_memo ? &memo : nullptr;
@@ -140,7 +139,7 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
                 if (stat <= a.threshold) ++hits;  // _kernels.py:275-276
                 if (a.stats) a.stats[local * a.reps + rep] = stat;
             }
-            if (rep1 == a.reps) store_state(a.cur + 6 * w, s);
+            if (a.store_final) store_state(a.cur + 6 * w, s);
             if (a.item_counts) atomicAdd((unsigned long long *)(a.item_counts + local),
                                          (unsigned long long)hits);
         }
@@ -155,6 +154,19 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         v = __reduce_add_sync(0xffffffffu, v);
         if (threadIdx.x == 0 && v) atomicAdd(a.count, (unsigned long long)v);
     }
+}
+
+// Chunked launches: no thread of the sampling kernel writes a state (the
+// item's chunks all read its start state, and nothing orders thread blocks);
+// afterwards every item advances by exactly reps * (I-1)(J-1) draws (one
+// uniform per free cell, _kernels.py:210-212), J = A^(reps F), in this kernel.
+__global__ void __launch_bounds__(256) advance_states_kernel(int64_t *cur, int64_t lo, int64_t hi,
+                                                             const Jump jump) {
+    const int64_t w = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= hi) return;
+    Mrg s = load_state(cur + 6 * w);
+    apply(jump, s);
+    store_state(cur + 6 * w, s);
 }
 
 __global__ void rcont2_kernel(const int32_t *rowm, const int32_t *colm, int nr, int nc, int ntot,
@@ -471,16 +483,12 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     jump_pow(0, &jl.j[0]);
     for (int64_t c = 1; c < nchunks; ++c) jump_mul(jl.j[c - 1], step, &jl.j[c]);
     const bool large = nchunks > kMaxChunks;
-    StateSnapshot snap;
-    StateIO io;
-    if (int rc = make_state_io(d_cur, item_lo, item_hi, nchunks > 1, st, snap, &io)) return rc;
     ChunkJumps jumps;
     if (!large) memcpy(jumps.j, jl.j, sizeof(Jump) * (size_t)nchunks);
 
     FisherArgs a;
-    a.cur = io.out;
-    a.cur_in = io.in;
-    a.cur_in_lo = io.in_lo;
+    a.cur = d_cur;
+    a.store_final = nchunks == 1 ? 1 : 0;
     a.rowm = rowm;
     a.colm = colm;
     a.lf = lfd;
@@ -539,6 +547,13 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
             e = launch_fisher<false, 1>(blocks, smem, st, a, jumps);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess && nchunks > 1) {
+        Jump total;
+        jump_pow((uint64_t)reps * (uint64_t)F, &total);
+        advance_states_kernel<<<(unsigned)ceil_div(nloc, 256), 256, 0, st>>>(d_cur, item_lo,
+                                                                             item_hi, total);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher kernel launch: %s", cudaGetErrorString(e));
     in.done(st);
     return SFB_OK;

@@ -1,8 +1,9 @@
 """Chunked launches must not depend on thread-block scheduling order.
 
 Several threads share one stream (each jumps ahead to its chunk) and the
-stream's last chunk writes its final state; the start states are therefore
-read from a snapshot (csrc/fill.cu make_state_io).  This test replays small,
+stream's final state must not be written while they read its start state:
+fills read a snapshot (csrc/fill.cu make_state_io), chunked Fisher launches
+advance the states in a second kernel (csrc/fisher.cu advance_states_kernel).  This test replays small,
 heavily chunked Fisher and fill launches under `compute-sanitizer --tool
 synccheck`, which perturbs block scheduling, and requires every run to equal
 a plain run (tools/determinism_check.py; without the snapshot the Fisher case
