@@ -19,11 +19,10 @@
  *   - stream states use the reference layout: int64 (n, 6) C-contiguous,
  *     row w = (g1[0..2], g2[0..2]) newest-first (core.py:161-172), mutated in
  *     place exactly where the reference kernels mutate `cur`;
- *   - results never depend on thread-block scheduling: a fill that splits a
- *     stream's draws over several threads reads start states from a
- *     stream-ordered snapshot of its state rows (cudaMallocAsync on the
- *     device's default pool, 48 bytes per stream, freed after the kernel); a
- *     chunked Fisher launch advances the states in a second kernel.
+ *   - results never depend on thread-block scheduling: a launch that splits a
+ *     stream's draws over several threads writes no state in its sampling
+ *     kernel; a second kernel on the same stream advances each stream by the
+ *     draws it consumed.
  */
 #ifndef SFB_H_
 #define SFB_H_

@@ -29,7 +29,6 @@
 #include <math.h>
 
 #include <algorithm>
-#include <atomic>
 
 #include "box_muller.cuh"
 #include "log1p_glibc.cuh"
@@ -652,43 +651,48 @@ static int zero_padding(void *out, size_t elsize, int64_t nrow, int64_t ncol, in
     return SFB_OK;
 }
 
-StateSnapshot::~StateSnapshot() {
-    if (buf) cudaFreeAsync(buf, st);
+// Chunked launches (several threads per stream): no thread writes a state --
+// a stream's chunks all read its start state and nothing orders thread
+// blocks -- and a second kernel then advances every stream of the launch by
+// the number of draws it consumed (each owned cell is exactly one draw; a
+// normal pair's two streams advance together, the discarded partner
+// included): one skip through the A^(2^b) table per stream.
+StateIO state_io(int64_t *cur, bool chunked) { return StateIO{cur, 0, chunked ? nullptr : cur}; }
+
+template <bool NORMAL>
+__global__ void __launch_bounds__(256) advance_fill_states(int64_t *cur, Geom g, int64_t lo,
+                                                           int64_t hi,
+                                                           const __grid_constant__ Pow2Table tab) {
+    const int64_t w = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= hi) return;
+    int64_t i, j;
+    if (NORMAL) {  // stream w of pair w / 2: grid row i, lane pair starting at column j
+        const int64_t p = w / 2, half = g.g1 / 2;
+        i = p / half;
+        j = 2 * (p % half);
+    } else {  // work item w = i + g0 j
+        i = w % g.g0;
+        j = w / g.g0;
+    }
+    const int64_t draws = owned(g.nrow, i, g.g0) * owned(g.ncol, j, g.g1);
+    if (draws == 0) return;
+    Mrg s = load_state(cur + 6 * w);
+    skip(tab, s, (uint64_t)draws);
+    store_state(cur + 6 * w, s);
 }
 
-int make_state_io(int64_t *cur, int64_t lo, int64_t hi, bool chunked, cudaStream_t st,
-                  StateSnapshot &snap, StateIO *io) {
-    io->out = cur;
-    io->in = cur;
-    io->in_lo = 0;
+static int finish_states(bool normal, bool chunked, int64_t *cur, const Geom &g, int64_t lo,
+                         int64_t hi, cudaStream_t st, const char *what) {
+    if (int rc = launch_check(what)) return rc;
     if (!chunked || hi <= lo) return SFB_OK;
-    // keep up to 1 GiB of freed snapshot memory in the device's default pool
-    // (otherwise it is returned to the driver at every synchronisation)
-    static std::atomic<uint64_t> pool_done{0};
-    int d = 0;
-    cudaGetDevice(&d);
-    if (!(pool_done.load() & (1ull << (d & 63)))) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
-            uint64_t keep = 0;
-            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            if (keep < (1ull << 30)) {
-                keep = 1ull << 30;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
-        }
-        pool_done.fetch_or(1ull << (d & 63));
-    }
-    const size_t bytes = (size_t)(hi - lo) * 6 * sizeof(int64_t);
-    cudaError_t e = cudaMallocAsync((void **)&snap.buf, bytes, st);
-    if (e == cudaSuccess) {
-        snap.st = st;
-        e = cudaMemcpyAsync(snap.buf, cur + 6 * lo, bytes, cudaMemcpyDeviceToDevice, st);
-    }
-    if (e != cudaSuccess) return fail(SFB_E_CUDA, "state snapshot: %s", cudaGetErrorString(e));
-    io->in = snap.buf;
-    io->in_lo = lo;
-    return SFB_OK;
+    Pow2Table tab;
+    pow2_table(&tab);
+    const unsigned nb = (unsigned)ceil_div(hi - lo, 256);
+    if (normal)
+        advance_fill_states<true><<<nb, 256, 0, st>>>(cur, g, lo, hi, tab);
+    else
+        advance_fill_states<false><<<nb, 256, 0, st>>>(cur, g, lo, hi, tab);
+    return launch_check("advance_fill_states");
 }
 
 template <int KIND>
@@ -740,10 +744,7 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
             qchunks = ceil_div(rows, qrpc);
             const int64_t qunits = qbase * qchunks;
             const unsigned qb = (unsigned)ceil_div(qunits, kThreads);
-            StateSnapshot snap;
-            StateIO io;
-            if (int rc = make_state_io(cur, item_lo, item_hi, qchunks > 1, st, snap, &io))
-                return rc;
+            const StateIO io = state_io(cur, qchunks > 1);
             // register cap / single-step variants (tuning); the exponential's
             // twelve log1p evaluations in flight want 3 CTAs/SM (measured 19.4 ->
             // 15.4 ms on C5), the store-bound kinds the uncapped default
@@ -770,11 +771,10 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
                     fill_uniform_quad<KIND, 1><<<qb, kThreads, 0, st>>>(io, out, g, j_lo, nquads,
                                                                         qrpc, qunits, rate, tab);
             }
-            return launch_check("fill_uniform_quad");
+            return finish_states(false, qchunks > 1, cur, g, item_lo, item_hi, st,
+                                 "fill_uniform_quad");
         }
-        StateSnapshot snap;
-        StateIO io;
-        if (int rc = make_state_io(cur, item_lo, item_hi, nchunks > 1, st, snap, &io)) return rc;
+        const StateIO io = state_io(cur, nchunks > 1);
         if ((v >> 12) & 3) {  // bits 12-13: 512 / 1024 threads per CTA
             const int nt = (v >> 12) == 1 ? 512 : 1024;
             const unsigned b2 = (unsigned)ceil_div(nunits, nt);
@@ -784,7 +784,8 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
             else
                 fill_uniform_fast<KIND, 1, 1024><<<b2, 1024, 0, st>>>(io, out, g, j_lo, npairs,
                                                                      rpc, nunits, rate, tab);
-            return launch_check("fill_uniform_fast");
+            return finish_states(false, nchunks > 1, cur, g, item_lo, item_hi, st,
+                                 "fill_uniform_fast");
         }
         switch ((v >> 4) & 15) {
             case 4:
@@ -804,7 +805,8 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
                                                                            npairs, rpc, nunits,
                                                                            rate, tab);
         }
-        return launch_check("fill_uniform_fast");
+        return finish_states(false, nchunks > 1, cur, g, item_lo, item_hi, st,
+                             "fill_uniform_fast");
     }
     // items with owned cells: rows i < min(g0, nrow), columns j < min(g1, ncol)
     GenMap m{};
@@ -822,12 +824,11 @@ static int launch_uniform(int64_t *cur, void *out, const Geom &g, int64_t item_l
     m.chunk = std::min(m.chunk, std::max<int64_t>(1, maxdraws));
     m.nchunks = ceil_div(maxdraws, m.chunk);
     m.nunits = ieff * m.J * m.nchunks;
-    StateSnapshot snap;
-    StateIO io;
-    if (int rc = make_state_io(cur, item_lo, item_hi, m.nchunks > 1, st, snap, &io)) return rc;
+    const StateIO io = state_io(cur, m.nchunks > 1);
     fill_uniform_generic<KIND><<<(unsigned)ceil_div(m.nunits, kThreads), kThreads, 0, st>>>(
         io, out, g, m, rate, tab);
-    return launch_check("fill_uniform_generic");
+    return finish_states(false, m.nchunks > 1, cur, g, item_lo, item_hi, st,
+                         "fill_uniform_generic");
 }
 
 // variant knob (tuning only): bit 0 -> cap registers (4 CTAs/SM), bit 3 ->
@@ -893,14 +894,13 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
         // one pair per thread where two would fit: twice the units
         const int64_t nu = (two && !use_two) ? nunits * 2 : nunits;
         const int minb = (v & 1) ? 4 : (v & 8) ? 3 : 1;
-        StateSnapshot snap;
-        StateIO io;
-        if (int rc = make_state_io(cur, item_lo, item_hi, nchunks > 1, st, snap, &io)) return rc;
+        const StateIO io = state_io(cur, nchunks > 1);
         if (v & 4)
             launch_normal_fast<T, false>(use_two, minb, st, io, out, g, i_lo, nrows_grid, rpc, nu);
         else
             launch_normal_fast<T, true>(use_two, minb, st, io, out, g, i_lo, nrows_grid, rpc, nu);
-        return launch_check("fill_normal_fast");
+        return finish_states(true, nchunks > 1, cur, g, item_lo, item_hi, st,
+                             "fill_normal_fast");
     }
     // pairs with owned cells: grid rows of the shard below min(g0, nrow),
     // pair columns jp with 2 jp < ncol
@@ -927,9 +927,7 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
     m.nunits = (i_end - m.i_lo) * m.J * m.nchunks;
     const bool paired = g.npad % 2 == 0 && ((uintptr_t)out % (2 * sizeof(T))) == 0;
     const unsigned nb = (unsigned)ceil_div(m.nunits, kThreads);
-    StateSnapshot snap;
-    StateIO io;
-    if (int rc = make_state_io(cur, item_lo, item_hi, m.nchunks > 1, st, snap, &io)) return rc;
+    const StateIO io = state_io(cur, m.nchunks > 1);
     const bool exact = tune_knob("SFB_NORMAL_VARIANT", normal_variant_default<T>()) & 4;
     if (exact)
         paired ? fill_normal_generic<T, false, true><<<nb, kThreads, 0, st>>>(io, out, g, m, tab)
@@ -937,7 +935,8 @@ static int launch_normal(int64_t *cur, T *out, const Geom &g, int64_t item_lo, i
     else
         paired ? fill_normal_generic<T, true, true><<<nb, kThreads, 0, st>>>(io, out, g, m, tab)
                : fill_normal_generic<T, true, false><<<nb, kThreads, 0, st>>>(io, out, g, m, tab);
-    return launch_check("fill_normal_generic");
+    return finish_states(true, m.nchunks > 1, cur, g, item_lo, item_hi, st,
+                         "fill_normal_generic");
 }
 
 }  // namespace sfb

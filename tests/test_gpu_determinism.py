@@ -2,12 +2,12 @@
 
 Several threads share one stream (each jumps ahead to its chunk) and the
 stream's final state must not be written while they read its start state:
-fills read a snapshot (csrc/fill.cu make_state_io), chunked Fisher launches
-advance the states in a second kernel (csrc/fisher.cu advance_states_kernel).  This test replays small,
+chunked launches write no state and a second kernel advances the streams
+(csrc/fill.cu advance_fill_states, csrc/fisher.cu advance_states_kernel).  This test replays small,
 heavily chunked Fisher and fill launches under `compute-sanitizer --tool
 synccheck`, which perturbs block scheduling, and requires every run to equal
-a plain run (tools/determinism_check.py; without the snapshot the Fisher case
-differed in 1 of 5 to 29 of 29 runs).
+a plain run (tools/determinism_check.py; with in-kernel state writes the
+Fisher case differed in 1 of 5 to 29 of 29 runs).
 """
 
 import os
