@@ -162,6 +162,11 @@ def require_device():
 
 
 def stream_handle():
+    """cudaStream_t of torch's current stream on the current device (the raw
+    query costs ~0.1 us; building a torch.cuda.Stream object ~3 us)."""
     import torch
 
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream

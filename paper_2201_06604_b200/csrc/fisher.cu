@@ -477,11 +477,19 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     nchunks = ceil_div(reps, rpc);
     // J_c = A^(c rpc F): one exact power, then one product per chunk; up to
     // kMaxChunks in the small parameter block, else the large one
+    // (cached per thread for the last (rpc F, nchunks): repeated calls on one
+    // table -- Monte Carlo loops -- skip the modular matrix products)
     thread_local ChunkJumpsLarge jl;
-    Jump step;
-    jump_pow((uint64_t)(rpc * F), &step);
-    jump_pow(0, &jl.j[0]);
-    for (int64_t c = 1; c < nchunks; ++c) jump_mul(jl.j[c - 1], step, &jl.j[c]);
+    thread_local uint64_t jl_step = ~0ull;
+    thread_local int64_t jl_n = 0;
+    if (jl_step != (uint64_t)(rpc * F) || jl_n < nchunks) {
+        Jump step;
+        jump_pow((uint64_t)(rpc * F), &step);
+        jump_pow(0, &jl.j[0]);
+        for (int64_t c = 1; c < nchunks; ++c) jump_mul(jl.j[c - 1], step, &jl.j[c]);
+        jl_step = (uint64_t)(rpc * F);
+        jl_n = nchunks;
+    }
     const bool large = nchunks > kMaxChunks;
     ChunkJumps jumps;
     if (!large) memcpy(jumps.j, jl.j, sizeof(Jump) * (size_t)nchunks);
@@ -548,8 +556,12 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && nchunks > 1) {
-        Jump total;
-        jump_pow((uint64_t)reps * (uint64_t)F, &total);
+        thread_local Jump total;
+        thread_local uint64_t total_n = ~0ull;
+        if (total_n != (uint64_t)reps * (uint64_t)F) {
+            jump_pow((uint64_t)reps * (uint64_t)F, &total);
+            total_n = (uint64_t)reps * (uint64_t)F;
+        }
         advance_states_kernel<<<(unsigned)ceil_div(nloc, 256), 256, 0, st>>>(d_cur, item_lo,
                                                                              item_hi, total);
         e = cudaGetLastError();
