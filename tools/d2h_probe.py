@@ -1,3 +1,5 @@
+"""D2H bandwidth of a 4 GiB device buffer into pinned memory: one copy vs row chunks on
+two copy streams (the MatrixBuffer.download strategy)."""
 import torch, time
 n = 4 << 30  # 4 GiB
 src = torch.empty(n, dtype=torch.uint8, device='cuda')

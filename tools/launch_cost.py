@@ -1,3 +1,5 @@
+"""Host-side cost of the Fisher launch path: Python wrapper vs raw ctypes enqueue,
+the stream-handle query, and the count readback variants."""
 import sys, time, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 import paper_2201_06604_b200 as sf
