@@ -19,19 +19,6 @@ LIB_PATH = os.path.join(_HERE, "libsfb.so")
 
 SFB_F64, SFB_F32, SFB_I64 = 0, 1, 2
 
-_ERRORS = {
-    -1: errors.InvalidArgumentError,
-    -2: errors.InsufficientStreamsError,
-    -3: errors.InvalidGridError,
-    -4: errors.InvalidRateError,
-    -5: errors.InvalidMarginsError,
-    -6: errors.InvalidSeedError,
-    -7: errors.CorruptStreamFileError,
-    -8: OSError,
-    -9: errors.InvalidParamsError,
-    -100: errors.DeviceError,
-}
-
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _f64p = ctypes.POINTER(ctypes.c_double)
 _f32p = ctypes.POINTER(ctypes.c_float)
@@ -108,7 +95,7 @@ def lib():
 def check(rc: int):
     if rc != 0:
         msg = lib().sfb_last_error().decode(errors="replace")
-        raise _ERRORS.get(rc, errors.DeviceError)(msg)
+        raise errors.from_status(rc, msg)
 
 
 def ptr(a, t=_i64p):
