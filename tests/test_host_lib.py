@@ -519,3 +519,24 @@ def test_device_fisher_sampler_large_margins():
     cnt, rcnt, cur, ref, st, rst = _host_fisher(t, 0, 8, reps_override=3, stats=True)
     assert time.time() - t0 < 60
     assert cnt == rcnt and np.array_equal(cur, ref) and np.array_equal(st, rst)
+
+
+def test_status_codes_match_header():
+    """Every SFB_E_* code in include/sfb.h maps to the exception class its
+    comment names (errors.from_status is the only C-ABI -> Python mapping)."""
+    from paper_2201_06604_b200 import errors
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "sfb.h")).read()
+    rows = re.findall(r"#define SFB_E_(\w+) \((-\d+)\)\s+/\* (.*?) \*/", hdr)
+    assert len(rows) == 10
+    for name, code, comment in rows:
+        exc = errors.from_status(int(code), name)
+        if name == "IO":
+            assert type(exc) is OSError
+        elif name == "CUDA":
+            assert type(exc) is errors.DeviceError
+        else:
+            assert type(exc).__name__ in comment, (name, type(exc))
+            assert isinstance(exc, errors.StreamforgeError) and exc.status == int(code)
+    assert type(errors.from_status(-12345, "x")) is errors.DeviceError
