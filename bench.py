@@ -425,13 +425,27 @@ def cpu_fisher(table, n_items, reps, g=(256, 64)):
     return n_items * reps / dt
 
 
+def c5_sample_rows(steps, warmup):
+    """the reference's generation timed at full size
+    when 34 GB of RAM is free (65536 rows), else at 1/16 (rows [0, 4096)).
+    Full size also needs the run to stay within a few minutes (~10 s per full
+    step on 16 cores): at most 24 steps + warm-ups."""
+    import psutil
+
+    free = psutil.virtual_memory().available
+    need = C5["nrow"] * C5["ncol"] * 8 + (4 << 30)  # output + states / headroom
+    full = free >= need and steps + warmup <= 24
+    return (C5["nrow"] if full else C5["nrow"] // 16), free
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return
     from oracle import oracle as orc
 
     orc.lib()
-    rows = 2048
+    rows, free = c5_sample_rows(args.steps, args.warmup)
+    frac = rows / C5["nrow"]
     n = rows * C5["ncol"]
     numba_fill = numba_fill_sampler(rows)
     kind = "reference" if numba_fill else "port"
@@ -444,27 +458,37 @@ def reference_arm(args, rank, world):
         vals.append(sample())
     total = time.perf_counter() - t0
     v = n * args.steps / sum(vals)
+    if rows == C5["nrow"]:
+        config = {"workload": "C5 runifGpu: 2^20 MRG31k3p streams x 4096 float64 uniforms "
+                              "(65536x65536 on WorkGrid(1024,1024)), one fill per step",
+                  "streams": C5["n_streams"], "uniforms_per_step": n}
+    else:
+        config = {"workload": f"C5 runifGpu at 1/16 (BASELINE.md 3: less than 34 GB of RAM "
+                              f"free): rows [0,{rows}) of the 65536x65536 matrix on "
+                              "WorkGrid(1024,1024), every stream",
+                  "streams": C5["n_streams"], "uniforms_per_step": n}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "uniforms/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C5 runifGpu (bounded CPU sample: rows [0,2048) of the "
-                                   "65536x65536 matrix on WorkGrid(1024,1024))",
-                       "streams": C5["n_streams"]},
+            "config": config,
+            "sample_fraction": frac, "host_ram_free_gb": free / 1e9,
+            "best_of_steps": n / min(vals),
             "cpu_baseline": {"value": v, "unit": "uniforms/s",
                              "cores": int(os.environ.get("NUMBA_NUM_THREADS", os.cpu_count()))
                              if kind == "reference" else orc.max_threads(),
                              "kind": kind,
-                             "sample": f"{n} uniforms per step (rows [0,{rows}) of C5), "
+                             "sample": f"{n} uniforms per step (rows [0,{rows}) of C5, "
+                                       f"fraction {frac:g}; {free / 1e9:.0f} GB RAM free), "
                                        + ("the unmodified reference's numba _kernels.fill_real "
                                           "from baseline/_ref" if kind == "reference" else
                                           "oracle C port of _kernels.fill_real (OpenMP)")
-                                       + ", all host cores"},
+                                       + ", all host cores, mean over the timed steps"},
             "e2e": {"value": v, "unit": "uniforms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     # the unmodified reference's own numbers where it is installed, the
     # oracle port's otherwise (both recorded)
-    nr = numba_reference(rows)
+    nr = numba_reference(2048)
     line["numba_reference"] = nr
     try:
         port = {"fisher_T4_tables_per_s": cpu_fisher(T4, 16384, 4),
@@ -509,15 +533,17 @@ def _import_reference():
 
 
 def numba_fill_sampler(rows):
-    """Callable timing one bounded C5 sample through the reference's own numba
-    kernel (baseline/_ref), or None when the reference is not installed."""
+    """Callable timing one C5 sample (rows [0, rows), all streams) through the
+    reference's own numba kernel (baseline/_ref), or None when the reference
+    is not installed."""
     K = _import_reference()
     if K is None:
         return None
     from oracle import oracle as orc
 
     states, _ = orc.create_streams((12345,) * 6, C5["n_streams"])
-    out = np.zeros((rows, C5["ncol"]))
+    out = np.empty((rows, C5["ncol"]))
+    out.fill(0.0)  # first touch outside the timed region (34 GB at full size)
     K.fill_real(states.copy(), out.ravel(), 64, C5["ncol"], C5["ncol"], C5["g0"], C5["g1"],
                 0, 1.0)  # JIT warm-up
 

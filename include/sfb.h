@@ -57,6 +57,14 @@ int sfb_version(void);
 /* 1 when the library was built for sm_100a and a device is visible */
 int sfb_device_ok(void);
 
+/* page-lock a host array in place for direct DMA of stream states (no
+ * reference counterpart: the reference never leaves the host).  Returns 0 when
+ * registered, 1 when the range is already page-locked (nothing done), or
+ * SFB_E_CUDA (not fatal: copies stay pageable); never leaves a sticky CUDA
+ * error behind. */
+int sfb_host_register(void *p, int64_t bytes);
+int sfb_host_unregister(void *p);
+
 /* ---- host stream arithmetic (exact integers; core.py) -------------------- */
 /* core.py:79-86 validate_seed -> SFB_E_INVALID_SEED */
 int sfb_validate_seed(const int64_t seed[6]);

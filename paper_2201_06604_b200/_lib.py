@@ -30,6 +30,8 @@ _SIGS = {
     "sfb_last_error": ([], ctypes.c_char_p),
     "sfb_version": ([], _int),
     "sfb_device_ok": ([], _int),
+    "sfb_host_register": ([_vp, _i64], _int),
+    "sfb_host_unregister": ([_vp], _int),
     "sfb_validate_seed": ([_i64p], _int),
     "sfb_next_state": ([_i64p, _i64p], _int),
     "sfb_jump_matrices": ([_int, _i64p, _i64p], _int),

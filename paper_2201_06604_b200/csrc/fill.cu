@@ -958,6 +958,29 @@ int sfb_device_ok(void) {
     return major == 10 && minor == 0;
 }
 
+int sfb_host_register(void *p, int64_t bytes) {
+    if (!p || bytes <= 0) return fail(SFB_E_INVALID_ARGUMENT, "nothing to register");
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost)
+        return 1;  // already page-locked (another registration or a pinned allocation)
+    cudaGetLastError();
+    cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // leave no sticky error behind: registration is optional
+        return fail(SFB_E_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+    }
+    return SFB_OK;
+}
+
+int sfb_host_unregister(void *p) {
+    cudaError_t e = cudaHostUnregister(p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SFB_E_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+    }
+    return SFB_OK;
+}
+
 int sfb_fill_real(int64_t *d_cur, int64_t n_streams, double *d_out, int64_t nrow, int64_t ncol,
                   int64_t npad, int64_t g0, int64_t g1, int mode, double rate, int64_t item_lo,
                   int64_t item_hi, int zero_pad, void *stream) {

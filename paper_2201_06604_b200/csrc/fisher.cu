@@ -66,12 +66,16 @@ struct FisherArgs {
     double threshold;
     int64_t item_lo, nloc, reps, rpc, nunits;
     int nr, nc, ntot, lf_len;
-    MemoSet memo;  // memoised first-row / first-column walks
-    int use_memo;
-    // small memo sets are staged into shared memory: the device block holding
-    // row | col | cfg | acc | k (16-byte aligned, memo_bytes long)
+    MemoSet memo;  // memoised walks (memo.on)
+    // the memo's cell descriptors (row | col | box, 16-byte aligned,
+    // memo_bytes long) are staged into shared memory; the records stay in
+    // global memory (L1/L2)
     const unsigned char *memo_blob;
     int memo_bytes;  // > 0: stage into shared memory
+    // WIDE launches (column work too large for shared memory): per-thread
+    // column work in global memory, jw[m * jstride + thread]
+    int *jwork_global;
+    int64_t jstride;
 };
 
 struct LfGlobal {
@@ -80,79 +84,106 @@ struct LfGlobal {
 };
 using LfShared = LfPlain;
 
-// dynamic shared memory: exp table (2 KiB) | margins | [lf] | jwork
-template <bool LF_SMEM, int MINB, int WALK, typename JUMPS = ChunkJumps>
+// One unit = (item, replicate chunk): its replicates on the item's stream
+// from the chunk's start state; returns the unit's hits.
+template <int WALK, typename LF, typename JUMPS>
+__device__ __forceinline__ unsigned long long run_unit(const FisherArgs &a, const JUMPS &jumps,
+                                                       int64_t u, const int32_t *rowm,
+                                                       const int32_t *colm, const LF &lf,
+                                                       const uint64_t *exptab, int *jw, int js,
+                                                       const MemoSet &memo) {
+    const int64_t local = u % a.nloc;
+    const int64_t c = u / a.nloc;
+    const int64_t w = a.item_lo + local;
+    const int64_t rep0 = c * a.rpc;
+    const int64_t rep1 = min(rep0 + a.rpc, a.reps);
+    unsigned long long uhits = 0;
+    if (rep0 >= rep1) return uhits;
+    Mrg s = load_state(a.cur + 6 * w);
+    if (c) apply(jumps.j[c], s);
+    for (int64_t rep = rep0; rep < rep1; ++rep) {
+        const double stat =
+            sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, lf, exptab, s, jw, js, nullptr, memo);
+        if (stat <= a.threshold) ++uhits;  // _kernels.py:275-276
+        if (a.stats) a.stats[local * a.reps + rep] = stat;
+    }
+    if (a.store_final) store_state(a.cur + 6 * w, s);
+    if (a.item_counts && uhits) atomicAdd((unsigned long long *)(a.item_counts + local), uhits);
+    return uhits;
+}
+
+// dynamic shared memory (byte offsets from the one extern array, so every
+// access compiles to LDS/STS): exp table (2 KiB) | margins | [lf] | column
+// work | memo cell descriptors.  WIDE: exp table only; margins, lf, column
+// work and memo descriptors in global memory, units visited grid-stride (the
+// grid is sized to the global column-work allocation).  Hits are counted in
+// 64 bits end to end (the reference counts in int64, _kernels.py:185,195,279).
+template <bool LF_SMEM, int MINB, int WALK, typename JUMPS = ChunkJumps, bool WIDE = false>
 __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const FisherArgs a,
                                                          const __grid_constant__ JUMPS jumps) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *exptab = (uint64_t *)smem;
-    int32_t *rowm = (int32_t *)(exptab + 256);
-    int32_t *colm = rowm + a.nr;
-    double *lfs = (double *)(((uintptr_t)(colm + a.nc) + 15) & ~(uintptr_t)15);
-    int *jwork = LF_SMEM ? (int *)(lfs + a.lf_len) : (int *)lfs;
-
     static const uint64_t kTab[256] = SFB_EXP_TABLE_INIT;
     for (int t = threadIdx.x; t < 256; t += blockDim.x) exptab[t] = kTab[t];
-    for (int t = threadIdx.x; t < a.nr; t += blockDim.x) rowm[t] = a.rowm[t];
-    for (int t = threadIdx.x; t < a.nc; t += blockDim.x) colm[t] = a.colm[t];
-    if (LF_SMEM)
-        for (int t = threadIdx.x; t < a.lf_len; t += blockDim.x) lfs[t] = a.lf[t];
-    __syncthreads();
-
-    // small memo sets: one cooperative copy into shared memory, pointers rebased
-    MemoSet memo = a.memo;
-    if (a.memo_bytes > 0) {
-        uint4 *dst = (uint4 *)(((uintptr_t)(jwork + (a.nc > 1 ? a.nc - 1 : 1) * blockDim.x) + 15) &
-                               ~(uintptr_t)15);
-        const uint4 *src = (const uint4 *)a.memo_blob;
-        for (int t = threadIdx.x; t < (a.memo_bytes + 15) / 16; t += blockDim.x) dst[t] = src[t];
-        const unsigned char *base = (const unsigned char *)dst;
-        auto rebase = [&](const void *p) { return base + ((const unsigned char *)p - a.memo_blob); };
-        memo.row = (const MemoCellDesc *)rebase(a.memo.row);
-        memo.col = (const MemoCellDesc *)rebase(a.memo.col);
-        memo.cfg = (const MemoConfig *)rebase(a.memo.cfg);
-        memo.acc = (const double *)rebase(a.memo.acc);
-        memo.k = (const int32_t *)rebase(a.memo.k);
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long hits = 0;
+    if constexpr (WIDE) {
         __syncthreads();
-    }
-    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int hits = 0;
-    if (u < a.nunits) {
-        const int64_t local = u % a.nloc;
-        const int64_t c = u / a.nloc;
-        const int64_t w = a.item_lo + local;
-        const int64_t rep0 = c * a.rpc;
-        const int64_t rep1 = min(rep0 + a.rpc, a.reps);
-        if (rep0 < rep1) {
-            Mrg s = load_state(a.cur + 6 * w);
-            if (c) apply(jumps.j[c], s);
-            int *jw = jwork + threadIdx.x;
-            const MemoSet *mp = a.use_memo ? &memo : nullptr;
-            for (int64_t rep = rep0; rep < rep1; ++rep) {
-                double stat;
-                if (LF_SMEM)
-                    stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, LfShared{lfs}, exptab, s,
-                                        jw, blockDim.x, nullptr, mp);
-                else
-                    stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, LfGlobal{a.lf}, exptab,
-                                        s, jw, blockDim.x, nullptr, mp);
-                if (stat <= a.threshold) ++hits;  // _kernels.py:275-276
-                if (a.stats) a.stats[local * a.reps + rep] = stat;
-            }
-            if (a.store_final) store_state(a.cur + 6 * w, s);
-            if (a.item_counts) atomicAdd((unsigned long long *)(a.item_counts + local),
-                                         (unsigned long long)hits);
+        const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t u = gtid; u < a.nunits; u += gstride)
+            hits += run_unit<WALK>(a, jumps, u, a.rowm, a.colm, LfGlobal{a.lf}, exptab,
+                                   a.jwork_global + gtid, (int)a.jstride, a.memo);
+    } else {
+        const size_t off_row = 2048;
+        const size_t off_col = off_row + 4 * (size_t)a.nr;
+        const size_t off_lf = (off_col + 4 * (size_t)a.nc + 15) & ~(size_t)15;
+        const size_t off_jw = off_lf + (LF_SMEM ? 8 * (size_t)a.lf_len : 0);
+        const size_t off_memo =
+            (off_jw + 4 * (size_t)(a.nc > 1 ? a.nc - 1 : 1) * blockDim.x + 15) & ~(size_t)15;
+        int32_t *srow = (int32_t *)(smem + off_row);
+        int32_t *scol = (int32_t *)(smem + off_col);
+        double *lfs = (double *)(smem + off_lf);
+        for (int t = threadIdx.x; t < a.nr; t += blockDim.x) srow[t] = a.rowm[t];
+        for (int t = threadIdx.x; t < a.nc; t += blockDim.x) scol[t] = a.colm[t];
+        if (LF_SMEM)
+            for (int t = threadIdx.x; t < a.lf_len; t += blockDim.x) lfs[t] = a.lf[t];
+        // the memo's cell descriptors: one cooperative copy, pointers rebased
+        MemoSet memo = a.memo;
+        if (memo.on) {
+            uint4 *dst = (uint4 *)(smem + off_memo);
+            const uint4 *src = (const uint4 *)a.memo_blob;
+            for (int t = threadIdx.x; t < (a.memo_bytes + 15) / 16; t += blockDim.x) dst[t] = src[t];
+            const unsigned char *blob = a.memo_blob;
+            memo.row = (const MemoCellDesc *)(smem + off_memo +
+                                              ((const unsigned char *)a.memo.row - blob));
+            memo.col = (const MemoCellDesc *)(smem + off_memo +
+                                              ((const unsigned char *)a.memo.col - blob));
+            if (a.memo.box)
+                memo.box = (const MemoBox *)(smem + off_memo +
+                                             ((const unsigned char *)a.memo.box - blob));
+        }
+        __syncthreads();
+        if (gtid < a.nunits) {  // one unit per thread
+            int *jw = (int *)(smem + off_jw) + threadIdx.x;
+            if (LF_SMEM)
+                hits = run_unit<WALK>(a, jumps, gtid, srow, scol, LfShared{lfs}, exptab, jw,
+                                      (int)blockDim.x, memo);
+            else
+                hits = run_unit<WALK>(a, jumps, gtid, srow, scol, LfGlobal{a.lf}, exptab, jw,
+                                      (int)blockDim.x, memo);
         }
     }
-    // warp shuffle -> shared -> one atomic per CTA
-    __shared__ int warp_sums[kFisherThreads / 32];
-    const int ws = __reduce_add_sync(0xffffffffu, hits);
-    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = ws;
+    // warp shuffle -> shared -> one atomic per CTA, all in 64 bits
+    __shared__ unsigned long long warp_sums[kFisherThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hits += __shfl_down_sync(0xffffffffu, hits, o);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = hits;
     __syncthreads();
     if (threadIdx.x < 32) {
-        int v = threadIdx.x < (blockDim.x >> 5) ? warp_sums[threadIdx.x] : 0;
-        v = __reduce_add_sync(0xffffffffu, v);
-        if (threadIdx.x == 0 && v) atomicAdd(a.count, (unsigned long long)v);
+        unsigned long long v = threadIdx.x < (blockDim.x >> 5) ? warp_sums[threadIdx.x] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0 && v) atomicAdd(a.count, v);
     }
 }
 
@@ -169,12 +200,14 @@ __global__ void __launch_bounds__(256) advance_states_kernel(int64_t *cur, int64
     store_state(cur + 6 * w, s);
 }
 
+// jw_global: column work for tables too wide for shared memory (else null)
 __global__ void rcont2_kernel(const int32_t *rowm, const int32_t *colm, int nr, int nc, int ntot,
-                              const double *lf, int64_t *state, int64_t *mat) {
+                              const double *lf, int64_t *state, int64_t *mat, int *jw_global) {
     static const uint64_t kTab[256] = SFB_EXP_TABLE_INIT;
     __shared__ uint64_t exptab[256];
     for (int t = 0; t < 256; ++t) exptab[t] = kTab[t];
-    extern __shared__ int jw[];
+    extern __shared__ int jw_smem[];
+    int *jw = jw_global ? jw_global : jw_smem;
     Mrg s = load_state(state);
     if (nr == 1) {  // _kernels.py:307-312: forced without draws
         for (int m = 0; m < nc; ++m) mat[m] = colm[m];
@@ -213,22 +246,37 @@ static int check_margins(const int64_t *nrowt, int nr, const int64_t *ncolt, int
     return SFB_OK;
 }
 
-// Per-device cache of the kernel inputs (int32 margins + lf table).  The
-// reference recomputes nothing between replicates, and a fisher_sim call with
-// the same table re-uploads nothing here either: the packed bytes are compared
-// with the last upload and the device copy is reused.  New content goes through
-// a grow-only pinned staging buffer (truly async copy) into a grow-only device
-// buffer; before overwriting, the event recorded after the last kernel that
-// read the buffer is awaited.  The lock is held across the launch, so calls on
-// one device serialise their use of the buffer.
-struct InputCache {
-    std::mutex mu;
+// Per-device LRU cache of the kernel inputs (int32 margins + lf table + memo
+// tables) for the last kInputCacheEntries tables.  The reference recomputes
+// nothing between replicates, and a fisher_sim call on a table seen recently
+// re-uploads nothing here either: the packed bytes are compared with each
+// entry's and a matching device copy is reused.  New content goes through the
+// entry's pinned staging buffer (truly async copy) into its device buffer.
+// Stream safety:
+//   * every entry records `uploaded` after its upload; a call that reuses the
+//     entry on any stream first makes that stream wait for it;
+//   * every launch that reads an entry records a per-stream `reader` event;
+//     before an entry is overwritten all its readers (every stream) and its
+//     last upload (the pinned buffer) are awaited.
+// The lock is held from lookup to the record of the launch (StagedInputs::done),
+// so no entry is evicted between staging and enqueue.
+constexpr int kInputCacheEntries = 4;
+
+struct InputEntry {
     std::vector<unsigned char> key;
     uint64_t memo_version = 0;
     unsigned char *dev = nullptr, *pinned = nullptr;
     size_t dev_cap = 0, pin_cap = 0;
-    cudaEvent_t last_use = nullptr;
-    bool pending = false;
+    cudaEvent_t uploaded = nullptr;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> readers;
+    uint64_t tick = 0;
+    bool valid = false;
+};
+
+struct InputCache {
+    std::mutex mu;
+    InputEntry e[kInputCacheEntries];
+    uint64_t tick = 0;
 };
 
 static InputCache &input_cache() {
@@ -240,22 +288,47 @@ static InputCache &input_cache() {
 
 struct StagedInputs {
     std::unique_lock<std::mutex> lock;
-    InputCache *cache = nullptr;
+    InputEntry *entry = nullptr;
     int32_t *rowm = nullptr, *colm = nullptr;
     double *lf = nullptr;
     MemoSet memo{};
     const unsigned char *memo_blob = nullptr;
     size_t memo_bytes = 0;
-    // record the consumer kernel (call after the launch)
+    // record the consumer kernel (call after the launch, lock still held)
     void done(cudaStream_t st) {
-        if (cache->last_use == nullptr)
-            cudaEventCreateWithFlags(&cache->last_use, cudaEventDisableTiming);
-        cudaEventRecord(cache->last_use, st);
-        cache->pending = true;
+        for (auto &r : entry->readers)
+            if (r.first == st) {
+                cudaEventRecord(r.second, st);
+                return;
+            }
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            cudaStreamSynchronize(st);  // no event: make the use complete now
+            return;
+        }
+        cudaEventRecord(ev, st);
+        entry->readers.emplace_back(st, ev);
     }
 };
 
 static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// wait for every reader and the last upload of an entry about to be rewritten
+static cudaError_t retire(InputEntry &en) {
+    cudaError_t e = cudaSuccess;
+    for (auto &r : en.readers) {
+        cudaError_t er = cudaEventSynchronize(r.second);
+        if (e == cudaSuccess) e = er;
+        cudaEventDestroy(r.second);
+    }
+    en.readers.clear();
+    if (en.uploaded) {
+        cudaError_t er = cudaEventSynchronize(en.uploaded);
+        if (e == cudaSuccess) e = er;
+    }
+    return e;
+}
 
 // Upload (or reuse) [margins | lf | memo tables] for this call.  The cache key
 // is the packed margins + lf bytes plus the memo version (memo tables are a
@@ -265,14 +338,15 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
                         const HostMemo *hm = nullptr, uint64_t memo_version = 0) {
     const size_t lf_off = align16((size_t)(nr + nc) * 4);
     const size_t key_bytes = lf_off + (size_t)lf_len * 8;
-    size_t row_off = align16(key_bytes), col_off = row_off, cfg_off = row_off,
-           acc_off = row_off, k_off = row_off, bytes = key_bytes;
+    // [margins | lf] [row | col | box] [records]
+    size_t row_off = align16(key_bytes), col_off = row_off, box_off = row_off,
+           rec_off = row_off, bytes = key_bytes;
     if (hm) {
         col_off = align16(row_off + hm->row.size() * sizeof(MemoCellDesc));
-        cfg_off = align16(col_off + hm->col.size() * sizeof(MemoCellDesc));
-        acc_off = align16(cfg_off + hm->cfg.size() * sizeof(MemoConfig));
-        k_off = align16(acc_off + hm->acc.size() * 8);
-        bytes = k_off + hm->k.size() * 4;
+        box_off = align16(col_off + hm->col.size() * sizeof(MemoCellDesc));
+        rec_off = align16(box_off + hm->box.size() * sizeof(MemoBox));
+        rec_off = (rec_off + 127) & ~(size_t)127;  // records start on a 128-byte line
+        bytes = rec_off + hm->rec.size() * 4;
     }
     thread_local std::vector<unsigned char> host;
     host.assign(key_bytes, 0);
@@ -282,97 +356,155 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
     memcpy(host.data() + lf_off, lf, (size_t)lf_len * 8);
     InputCache &c = input_cache();
     out.lock = std::unique_lock<std::mutex>(c.mu);
-    out.cache = &c;
-    if (c.key != host || c.memo_version != memo_version) {
-        cudaError_t e = cudaSuccess;
-        if (c.pending) e = cudaEventSynchronize(c.last_use);  // previous readers done
-        if (e == cudaSuccess && bytes + 64 > c.dev_cap) {
-            if (c.dev) cudaFree(c.dev);
-            c.dev_cap = std::max(bytes + 64, (size_t)1 << 20);  // +64: 16-byte block copies
-            e = cudaMalloc((void **)&c.dev, c.dev_cap);
+    InputEntry *hit = nullptr, *victim = &c.e[0];
+    for (InputEntry &en : c.e) {
+        if (en.valid && en.memo_version == memo_version && en.key == host) {
+            hit = &en;
+            break;
+        }
+        if (!en.valid ? victim->valid : (victim->valid && en.tick < victim->tick)) victim = &en;
+    }
+    cudaError_t e = cudaSuccess;
+    if (hit) {
+        // the upload may have been issued on another stream
+        e = cudaStreamWaitEvent(st, hit->uploaded, 0);
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher input wait: %s", cudaGetErrorString(e));
+    } else {
+        InputEntry &en = *victim;
+        hit = &en;
+        en.valid = false;
+        e = retire(en);  // readers on every stream + the pinned buffer
+        if (e == cudaSuccess && bytes + 64 > en.dev_cap) {
+            if (en.dev) cudaFree(en.dev);
+            en.dev = nullptr;
+            en.dev_cap = std::max(bytes + 64, (size_t)1 << 20);  // +64: 16-byte block copies
+            e = cudaMalloc((void **)&en.dev, en.dev_cap);
+            if (e != cudaSuccess) en.dev_cap = 0;
         }
         // uploaded in whole 16-byte blocks (the kernel's memo staging copies
         // uint4s), the tail zero-filled so no uninitialised byte is ever read
         const size_t up = align16(bytes);
-        if (e == cudaSuccess && up > c.pin_cap) {
-            if (c.pinned) cudaFreeHost(c.pinned);
-            c.pin_cap = std::max(up, (size_t)1 << 20);
-            e = cudaMallocHost((void **)&c.pinned, c.pin_cap);
+        if (e == cudaSuccess && up > en.pin_cap) {
+            if (en.pinned) cudaFreeHost(en.pinned);
+            en.pinned = nullptr;
+            en.pin_cap = std::max(up, (size_t)1 << 20);
+            e = cudaMallocHost((void **)&en.pinned, en.pin_cap);
+            if (e != cudaSuccess) en.pin_cap = 0;
         }
         if (e == cudaSuccess) {
-            memcpy(c.pinned, host.data(), key_bytes);
+            memcpy(en.pinned, host.data(), key_bytes);
             if (hm) {
-                memcpy(c.pinned + row_off, hm->row.data(), hm->row.size() * sizeof(MemoCellDesc));
-                memcpy(c.pinned + col_off, hm->col.data(), hm->col.size() * sizeof(MemoCellDesc));
-                memcpy(c.pinned + cfg_off, hm->cfg.data(), hm->cfg.size() * sizeof(MemoConfig));
-                memcpy(c.pinned + acc_off, hm->acc.data(), hm->acc.size() * 8);
-                memcpy(c.pinned + k_off, hm->k.data(), hm->k.size() * 4);
+                auto put = [&](size_t off, const void *src, size_t n) {
+                    if (n) memcpy(en.pinned + off, src, n);
+                };
+                memset(en.pinned + key_bytes, 0, bytes - key_bytes);  // alignment gaps
+                put(row_off, hm->row.data(), hm->row.size() * sizeof(MemoCellDesc));
+                put(col_off, hm->col.data(), hm->col.size() * sizeof(MemoCellDesc));
+                put(box_off, hm->box.data(), hm->box.size() * sizeof(MemoBox));
+                put(rec_off, hm->rec.data(), hm->rec.size() * 4);
             }
-            memset(c.pinned + bytes, 0, up - bytes);
-            e = cudaMemcpyAsync(c.dev, c.pinned, up, cudaMemcpyHostToDevice, st);
+            memset(en.pinned + bytes, 0, up - bytes);
+            e = cudaMemcpyAsync(en.dev, en.pinned, up, cudaMemcpyHostToDevice, st);
         }
-        if (e == cudaSuccess && c.last_use == nullptr)
-            e = cudaEventCreateWithFlags(&c.last_use, cudaEventDisableTiming);
-        if (e == cudaSuccess) {  // the pinned buffer is busy until this copy lands
-            e = cudaEventRecord(c.last_use, st);
-            c.pending = true;
-        }
+        if (e == cudaSuccess && en.uploaded == nullptr)
+            e = cudaEventCreateWithFlags(&en.uploaded, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(en.uploaded, st);
         if (e != cudaSuccess) {
-            c.key.clear();
-            c.dev_cap = c.dev ? c.dev_cap : 0;
+            cudaGetLastError();
             return fail(SFB_E_CUDA, "fisher input upload: %s", cudaGetErrorString(e));
         }
-        c.key = host;
-        c.memo_version = memo_version;
+        en.key = host;
+        en.memo_version = memo_version;
+        en.valid = true;
     }
-    out.rowm = (int32_t *)c.dev;
+    hit->tick = ++c.tick;
+    out.entry = hit;
+    unsigned char *dev = hit->dev;
+    out.rowm = (int32_t *)dev;
     out.colm = out.rowm + nr;
-    out.lf = (double *)(c.dev + lf_off);
+    out.lf = (double *)(dev + lf_off);
     if (hm) {
-        out.memo = MemoSet{(const MemoCellDesc *)(c.dev + row_off),
-                           (const MemoCellDesc *)(c.dev + col_off),
-                           (const MemoConfig *)(c.dev + cfg_off), (const double *)(c.dev + acc_off),
-                           (const int32_t *)(c.dev + k_off)};
-        out.memo_blob = c.dev + row_off;
-        out.memo_bytes = bytes - row_off;
+        out.memo = MemoSet{(const MemoCellDesc *)(dev + row_off),
+                           (const MemoCellDesc *)(dev + col_off),
+                           hm->box.empty() ? nullptr : (const MemoBox *)(dev + box_off),
+                           (const uint32_t *)(dev + rec_off), hm->rec.empty() ? 0 : 1};
+        out.memo_blob = dev + row_off;
+        out.memo_bytes = rec_off - row_off;  // the descriptors (staged per CTA)
     }
     return SFB_OK;
 }
 
-// Process-wide cache of the memo tables of the last table seen (building them
-// walks every tabulated configuration once on the host: tens of ms for T10).
-struct MemoCache {
-    std::mutex mu;
+// Process-wide LRU of the memo tables of the last kMemoCacheEntries tables
+// (building them walks every tabulated configuration once on the host: tens
+// of ms for T10).  Versions are unique per build, so input-cache entries of an
+// evicted memo set never match a rebuilt one.
+constexpr int kMemoCacheEntries = 4;
+
+struct MemoEntry {
     std::vector<int64_t> margins;
     std::vector<double> lf;
     std::shared_ptr<const HostMemo> memo;
-    uint64_t version = 0;
+    uint64_t version = 0, tick = 0;
+};
+
+struct MemoCache {
+    std::mutex mu;
+    MemoEntry e[kMemoCacheEntries];
+    uint64_t version = 0, tick = 0;
 };
 
 static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, const int64_t *ncolt,
                                                 int nc, int ntot, const double *lf, int64_t lf_len,
                                                 uint64_t *version) {
     static MemoCache mc;
-    std::lock_guard<std::mutex> g(mc.mu);
     std::vector<int64_t> key(nrowt, nrowt + nr);
     key.push_back(-1);
     key.insert(key.end(), ncolt, ncolt + nc);
-    if (!mc.memo || key != mc.margins || (int64_t)mc.lf.size() != lf_len ||
-        memcmp(mc.lf.data(), lf, (size_t)lf_len * 8) != 0) {
-        std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
-        auto hm = std::make_shared<HostMemo>();
-        build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
-                       kMemoMaxEntries, kMemoMaxSeq, kMemoSigmas);
-        mc.memo = hm;
-        mc.margins = key;
-        mc.lf.assign(lf, lf + lf_len);
-        ++mc.version;
+    {
+        std::lock_guard<std::mutex> g(mc.mu);
+        for (MemoEntry &en : mc.e)
+            if (en.memo && en.margins == key && (int64_t)en.lf.size() == lf_len &&
+                memcmp(en.lf.data(), lf, (size_t)lf_len * 8) == 0) {
+                en.tick = ++mc.tick;
+                *version = en.version;
+                return en.memo;
+            }
     }
-    *version = mc.version;
-    return mc.memo;
+    // build outside the lock (other tables' calls proceed meanwhile)
+    std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
+    auto hm = std::make_shared<HostMemo>();
+    build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
+                   kMemoMaxWords, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0);
+    std::lock_guard<std::mutex> g(mc.mu);
+    MemoEntry *victim = &mc.e[0];
+    for (MemoEntry &en : mc.e)
+        if (!en.memo ? victim->memo != nullptr : (victim->memo && en.tick < victim->tick))
+            victim = &en;
+    victim->margins = std::move(key);
+    victim->lf.assign(lf, lf + lf_len);
+    victim->memo = hm;
+    victim->version = ++mc.version;
+    victim->tick = ++mc.tick;
+    *version = victim->version;
+    return hm;
 }
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static int sm_count() {  // of the current device, cached
+    static std::atomic<int> cache[64];
+    int d = 0;
+    cudaGetDevice(&d);
+    int n = cache[d & 63].load();
+    if (!n) {
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = 148;
+        }
+        cache[d & 63].store(n);
+    }
+    return n;
+}
 
 template <bool LF_SMEM, int MINB, int WALK>
 static cudaError_t launch_fisher_walk(unsigned blocks, size_t smem, cudaStream_t st,
@@ -408,6 +540,15 @@ static cudaError_t launch_fisher_large(unsigned blocks, size_t smem, cudaStream_
         done_mask.fetch_or(bit);
     }
     fisher_kernel<LF_SMEM, MINB, kFisherWalkDefault, ChunkJumpsLarge>
+        <<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    return cudaGetLastError();
+}
+
+// tables whose column work does not fit in shared memory (any width; the
+// reference allocates jwork for any nc, _kernels.py:193-194)
+static cudaError_t launch_fisher_wide(unsigned blocks, size_t smem, cudaStream_t st,
+                                      const FisherArgs &a, const ChunkJumpsLarge &jumps) {
+    fisher_kernel<false, 4, kFisherWalkDefault, ChunkJumpsLarge, true>
         <<<blocks, kFisherThreads, smem, st>>>(a, jumps);
     return cudaGetLastError();
 }
@@ -466,11 +607,31 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     int32_t *rowm = in.rowm, *colm = in.colm;
     double *lfd = in.lf;
 
-    // chunking: enough units to fill the machine, bounded by kMaxChunks
+    // chunking: units = items x replicate chunks, one thread each.  The time
+    // is ~ (waves of resident threads) x (tables per thread + a per-unit
+    // start cost of ~half a table: state load, chunk jump), so the chunk
+    // count minimising that is taken (C3: 16384 items x 62 reps -> 9 chunks of
+    // 7 = 0.97 of a wave).  SFB_FISHER_TARGET_Q (tuning) instead aims at
+    // Q/4 x 148 x 2048 x 2 units.
     const int64_t F = (int64_t)(nr - 1) * (nc - 1);
-    // units to aim for, in quarters of 148 x 2048 x 2 (tuning knob)
-    const int64_t kTarget = 148LL * 2048 * 2 * tune_knob("SFB_FISHER_TARGET_Q", 4) / 4;
-    int64_t nchunks = std::min<int64_t>({(int64_t)kMaxChunksLarge, reps, ceil_div(kTarget, nloc)});
+    const int q_knob = tune_knob("SFB_FISHER_TARGET_Q", -1);
+    int64_t nchunks = 1;
+    if (q_knob > 0) {
+        const int64_t target = 148LL * 2048 * 2 * q_knob / 4;
+        nchunks = std::min<int64_t>({(int64_t)kMaxChunksLarge, reps, ceil_div(target, nloc)});
+    } else {
+        const int64_t resident = (int64_t)sm_count() * 4 * kFisherThreads;
+        double best = 0;
+        for (int64_t c = 1; c <= std::min<int64_t>(kMaxChunksLarge, reps); ++c) {
+            const int64_t r = ceil_div(reps, c);
+            if (c > 1 && ceil_div(reps, r) != c) continue;  // same rpc as a smaller c
+            const double cost = (double)ceil_div(nloc * c, resident) * ((double)r + 0.5);
+            if (c == 1 || cost < best) {
+                best = cost;
+                nchunks = c;
+            }
+        }
+    }
     if (F == 0) nchunks = 1;  // degenerate tables consume no draws
     nchunks = std::max<int64_t>(1, nchunks);
     const int64_t rpc = ceil_div(reps, nchunks);
@@ -514,29 +675,52 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     a.ntot = ntot;
     a.lf_len = (int)lf_len;
     a.memo = in.memo;
-    a.use_memo = use_memo ? 1 : 0;
+    if (!use_memo) a.memo = MemoSet{};
     a.memo_blob = in.memo_blob;
-    a.memo_bytes = 0;
+    a.memo_bytes = use_memo ? (int)in.memo_bytes : 0;
 
-    const size_t head = 2048 + (size_t)(nr + nc) * 4 + 16;
-    const size_t jw = (size_t)std::max(nc - 1, 1) * kFisherThreads * 4;
-    const size_t lf_bytes = (size_t)lf_len * 8;
-    const bool lf_smem = head + lf_bytes + jw <= 110 * 1024;
-    size_t smem = head + (lf_smem ? lf_bytes : 0) + jw;
-    // memo tables small enough to share the CTA's budget (T4: 22 KB) live in
-    // shared memory: their binary searches then cost ~30 instead of ~500 cycles
-    if (use_memo && in.memo_bytes > 0 &&
-        smem + 16 + in.memo_bytes <= (size_t)tune_knob("SFB_FISHER_MEMO_SMEM_KB", 48) * 1024) {
-        a.memo_bytes = (int)in.memo_bytes;
-        smem += 16 + in.memo_bytes;
+    // shared memory layout of fisher_kernel (same offsets): exp table |
+    // margins | [lf] | column work | memo cell descriptors; lf goes to global
+    // memory (read through L1) when the whole layout would pass ~110 KB
+    auto layout = [&](bool lf_in_smem) {
+        const size_t off_col = 2048 + 4 * (size_t)nr;
+        const size_t off_lf = align16(off_col + 4 * (size_t)nc);
+        const size_t off_jw = off_lf + (lf_in_smem ? 8 * (size_t)lf_len : 0);
+        const size_t off_memo = align16(off_jw + 4 * (size_t)std::max(nc - 1, 1) * kFisherThreads);
+        return off_memo + (size_t)a.memo_bytes;
+    };
+    const bool lf_smem = layout(true) <= 110 * 1024;
+    size_t smem = layout(lf_smem);
+    unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
+    a.jwork_global = nullptr;
+    a.jstride = 0;
+    const bool wide = smem > (size_t)kMaxFisherSmem;
+    if (wide) {
+        // column work in global memory: (nc-1) ints per thread, the grid capped
+        // so the allocation stays <= 256 MiB (units are visited grid-stride)
+        const int64_t per_thread = (int64_t)(nc - 1) * 4;
+        const int64_t cap = std::max<int64_t>(
+            kFisherThreads, ((int64_t)256 << 20) / per_thread / kFisherThreads * kFisherThreads);
+        const int64_t threads = std::min<int64_t>((int64_t)blocks * kFisherThreads, cap);
+        if ((int64_t)(nc - 1) * threads >= ((int64_t)1 << 31))
+            return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel (%d columns)",
+                        nc);
+        blocks = (unsigned)(threads / kFisherThreads);
+        e = cudaMallocAsync((void **)&a.jwork_global, (size_t)(threads * per_thread), st);
+        if (e != cudaSuccess)
+            return fail(SFB_E_CUDA, "fisher column work allocation: %s", cudaGetErrorString(e));
+        a.jstride = threads;
+        a.memo_bytes = 0;
+        smem = 2048;
     }
-    const unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
-    if (smem > (size_t)kMaxFisherSmem)
-        return fail(SFB_E_INVALID_ARGUMENT, "table too wide for the device kernel");
     // register cap: 4 CTAs/SM (64 regs) -- best for every table measured on
     // B200 (tools/tune.py sweep of 3 walk forms x {3, 4} CTAs/SM)
     const int minb = tune_knob("SFB_FISHER_MINB", 4);
-    if (large) {
+    if (wide) {
+        e = launch_fisher_wide(blocks, smem, st, a, jl);
+        cudaError_t ef = cudaFreeAsync(a.jwork_global, st);
+        if (e == cudaSuccess) e = ef;
+    } else if (large) {
         e = lf_smem ? launch_fisher_large<true, 4>(blocks, smem, st, a, jl)
                     : launch_fisher_large<false, 4>(blocks, smem, st, a, jl);
     } else if (lf_smem) {
@@ -578,9 +762,22 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
     cudaStream_t st = (cudaStream_t)stream;
     StagedInputs in;
     if (int rc = stage_inputs(nrowt, nr, ncolt, nc, lf, lf_len, st, in)) return rc;
-    rcont2_kernel<<<1, 1, (size_t)std::max(nc, 1) * 4, st>>>(in.rowm, in.colm, nr, nc, ntot, in.lf,
-                                                              d_state, d_mat);
-    cudaError_t e = cudaGetLastError();
+    // column work in shared memory up to 48 KiB, else a stream-ordered scratch
+    const size_t jw_bytes = (size_t)std::max(nc, 1) * 4;
+    int *jw_global = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (jw_bytes > 48 * 1024) {
+        e = cudaMallocAsync((void **)&jw_global, jw_bytes, st);
+        if (e != cudaSuccess)
+            return fail(SFB_E_CUDA, "rcont2 column work allocation: %s", cudaGetErrorString(e));
+    }
+    rcont2_kernel<<<1, 1, jw_global ? 0 : jw_bytes, st>>>(in.rowm, in.colm, nr, nc, ntot, in.lf,
+                                                          d_state, d_mat, jw_global);
+    e = cudaGetLastError();
+    if (jw_global) {
+        cudaError_t ef = cudaFreeAsync(jw_global, st);
+        if (e == cudaSuccess) e = ef;
+    }
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "rcont2 launch: %s", cudaGetErrorString(e));
     in.done(st);
     return SFB_OK;

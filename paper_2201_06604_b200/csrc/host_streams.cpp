@@ -658,9 +658,8 @@ int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const
     const bool use_memo = tune_knob("SFB_FISHER_MEMO", 1) != 0;
     if (use_memo)
         build_memo_set(rowm.data(), nr, colm.data(), nc, (int)ntot, LfPlain{lf}, kExpTable, hm,
-                       kMemoMaxEntries, kMemoMaxSeq, kMemoSigmas);
-    const MemoSet ms = hm.view();
-    const MemoSet *mp = use_memo ? &ms : nullptr;
+                       kMemoMaxWords, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0);
+    const MemoSet mp = use_memo ? hm.view() : MemoSet{};
     const int walk = tune_knob("SFB_FISHER_WALK", 3);
     int64_t hits = 0;
     for (int64_t w = item_lo; w < item_hi; ++w) {

@@ -113,26 +113,42 @@ struct Mat3 {
     uint32_t m[9];
 };
 
-// a*v0 + b*v1 + c*v2 mod m: three 62-bit products sum below 2^64
-SFB_HD uint32_t dot3_mod(const uint32_t *row, uint32_t v0, uint32_t v1, uint32_t v2,
-                         uint32_t mod) {
-    const uint64_t acc = (uint64_t)row[0] * v0 + (uint64_t)row[1] * v1 + (uint64_t)row[2] * v2;
-    return (uint32_t)(acc % mod);
+// a*v0 + b*v1 + c*v2: three products < 2^62 sum below 2^64
+SFB_HD uint64_t dot3(const uint32_t *row, uint32_t v0, uint32_t v1, uint32_t v2) {
+    return (uint64_t)row[0] * v0 + (uint64_t)row[1] * v1 + (uint64_t)row[2] * v2;
+}
+
+// x mod m1 for any 64-bit x, without a 64-bit division: 2^31 == 1 (mod m1),
+// so x == (x & m1) + (x >> 31) < 2^33 + 2^31, folded once more below 2 m1
+SFB_HD uint32_t mod_m1(uint64_t x) {
+    x = (x & kM1) + (x >> 31);
+    const uint32_t y = (uint32_t)(x & kM1) + (uint32_t)(x >> 31);  // < 2^31 + 8
+    return csub(y, kM1);
+}
+
+// x mod m2 for any 64-bit x: 2^31 == 21069 (mod m2), so
+// x == (x >> 31) * 21069 + (x & m1): < 2^33 * 21069 + 2^31 < 2^49, then
+// < (2^18 + 1) * 21069 + 2^31 < 2^33, then below 2 m2
+SFB_HD uint32_t mod_m2(uint64_t x) {
+    x = (x >> 31) * 21069u + (x & kM1);
+    x = (x >> 31) * 21069u + (x & kM1);
+    const uint32_t y = (uint32_t)(x >> 31) * 21069u + (uint32_t)(x & kM1);  // < 2^31 + 4 * 21069
+    return csub(y, kM2);
 }
 
 SFB_HD void apply1(const Mat3 &p, uint32_t &x0, uint32_t &x1, uint32_t &x2) {
-    const uint32_t y0 = dot3_mod(p.m + 0, x0, x1, x2, kM1);
-    const uint32_t y1 = dot3_mod(p.m + 3, x0, x1, x2, kM1);
-    const uint32_t y2 = dot3_mod(p.m + 6, x0, x1, x2, kM1);
+    const uint32_t y0 = mod_m1(dot3(p.m + 0, x0, x1, x2));
+    const uint32_t y1 = mod_m1(dot3(p.m + 3, x0, x1, x2));
+    const uint32_t y2 = mod_m1(dot3(p.m + 6, x0, x1, x2));
     x0 = y0;
     x1 = y1;
     x2 = y2;
 }
 
 SFB_HD void apply2(const Mat3 &p, uint32_t &x0, uint32_t &x1, uint32_t &x2) {
-    const uint32_t y0 = dot3_mod(p.m + 0, x0, x1, x2, kM2);
-    const uint32_t y1 = dot3_mod(p.m + 3, x0, x1, x2, kM2);
-    const uint32_t y2 = dot3_mod(p.m + 6, x0, x1, x2, kM2);
+    const uint32_t y0 = mod_m2(dot3(p.m + 0, x0, x1, x2));
+    const uint32_t y1 = mod_m2(dot3(p.m + 3, x0, x1, x2));
+    const uint32_t y2 = mod_m2(dot3(p.m + 6, x0, x1, x2));
     x0 = y0;
     x1 = y1;
     x2 = y2;

@@ -213,14 +213,20 @@ def launch_fill(kind, cur_dev, n_streams, out, nrow, ncol, npad, g0, g1, rate=1.
                 item_lo=0, item_hi=None, zero_pad=True, stream=None):
     """Enqueue one fill kernel on raw device buffers (the C-ABI seam).
     `cur_dev`: int64 (n,6) CUDA tensor; `out`: (nrow, npad) CUDA tensor."""
+    import torch
+
+    want = {"normal": (torch.float64, torch.float32), "uniform-integer": (torch.int64,),
+            "uniform": (torch.float64,), "exponential": (torch.float64,)}.get(kind)
+    if want is None:
+        raise InvalidArgumentError(f"unknown fill kind {kind!r}")
+    if out.dtype not in want:  # the kernels write 8-byte cells except float32 normals
+        raise InvalidArgumentError(f"{kind} fills cannot write a {out.dtype} buffer")
     L = _lib.lib()
     item_hi = g0 * g1 if item_hi is None else item_hi
     st = _lib.stream_handle() if stream is None else stream
     cp, op = _lib.dptr(cur_dev), _lib.dptr(out)
     zp = 1 if zero_pad else 0
     if kind == "normal":
-        import torch
-
         dt = _lib.SFB_F32 if out.dtype == torch.float32 else _lib.SFB_F64
         rc = L.sfb_fill_normal(cp, n_streams, op, dt, nrow, ncol, npad, g0, g1, item_lo,
                                item_hi, zp, st)
@@ -236,11 +242,10 @@ def launch_fill(kind, cur_dev, n_streams, out, nrow, ncol, npad, g0, g1, rate=1.
     _lib.check(rc)
 
 
-def run_grid(streams, grid, nrow, ncol, kind, rate=1.0, npad=None, threads=None, dtype=None):
-    """Fill an nrow x ncol matrix, advancing the used streams in place
-    (grid.py:112-144).  kind: "uniform", "uniform-integer", "exponential",
-    "normal".  `threads` is accepted for API compatibility and never changes
-    results.  `dtype` (extension): np.float32 for float32 normals."""
+def check_fill(streams, grid, kind, dtype=None) -> np.dtype:
+    """Validation of a fill request in the reference's order (grid.py:112-123):
+    streams, paired lanes for normals, the kind; then the output dtype of the
+    kind (float32 only for normals, the extension).  Returns the dtype."""
     _check_streams(streams, grid)
     if kind == "normal":
         grid.require_paired_lanes()
@@ -251,6 +256,15 @@ def run_grid(streams, grid, nrow, ncol, kind, rate=1.0, npad=None, threads=None,
         raise InvalidArgumentError(f"{kind} fills produce {np.dtype(KIND_DTYPES[kind])}")
     if kind == "normal" and out_dtype not in (np.dtype(np.float64), np.dtype(np.float32)):
         raise InvalidArgumentError("normal fills produce float64 or float32")
+    return out_dtype
+
+
+def run_grid(streams, grid, nrow, ncol, kind, rate=1.0, npad=None, threads=None, dtype=None):
+    """Fill an nrow x ncol matrix, advancing the used streams in place
+    (grid.py:112-144).  kind: "uniform", "uniform-integer", "exponential",
+    "normal".  `threads` is accepted for API compatibility and never changes
+    results.  `dtype` (extension): np.float32 for float32 normals."""
+    out_dtype = check_fill(streams, grid, kind, dtype)
     _lib.require_device()
     buf = MatrixBuffer.on_device(nrow, ncol, npad, dtype=out_dtype)
     cur = streams.device_current()

@@ -24,7 +24,7 @@ import numpy as np
 from . import _lib
 from .errors import InvalidArgumentError
 from .fisher import FisherResult, launch_fisher, plan_fisher
-from .grid import KIND_DTYPES, MatrixBuffer, _check_streams, launch_fill
+from .grid import MatrixBuffer, check_fill, launch_fill
 
 
 def shard_range(n_units: int, rank: int, world: int, align: int = 1):
@@ -160,12 +160,7 @@ def run_grid_sharded(streams, grid, nrow, ncol, kind, rate=1.0, npad=None, dtype
     start zeroed and are summed across ranks (disjoint cells), so every rank
     returns the full matrix; otherwise only the rank's own cells are valid."""
     dist = _dist()
-    _check_streams(streams, grid)
-    if kind == "normal":
-        grid.require_paired_lanes()
-    elif kind not in ("uniform-integer", "uniform", "exponential"):
-        raise InvalidArgumentError(f"unknown fill kind {kind!r}")
-    out_dtype = np.dtype(KIND_DTYPES[kind] if dtype is None else dtype)
+    out_dtype = check_fill(streams, grid, kind, dtype)
     executor = executor or DeviceExecutor()
     rank, world = _world(group)
     lo, hi = fill_shard(kind, grid.nglobal0, grid.nglobal1, rank, world)

@@ -506,6 +506,58 @@ def test_checkpoint_continuation_c5_full(tmp_path):
     b = sf.run_grid(st2, g, 32768, 65536, "uniform")
     assert torch.equal(b.tensor, full.tensor[32768:])
     assert st2 == st_full
+    # against the oracle, not only self-consistency: every final state is
+    # A^4096 s_w (4096 draws per stream), and sampled cells equal the oracle's
+    # skip-ahead draws (_kernels.py:50-80: item (i, j) = stream i + g0 j owns
+    # cells r = i mod g0, c = j mod g1, row-major)
+    seeds = oa.fresh_states(1 << 20)
+    assert np.array_equal(st_full.current, skip_all(seeds, 12))
+    rng = np.random.default_rng(2026)
+    rows = np.concatenate([rng.integers(0, 65536, 8192), [0, 0, 65535, 65535]])
+    cols = np.concatenate([rng.integers(0, 65536, 8192), [0, 65535, 0, 65535]])
+    got = full.tensor[torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()].cpu().numpy()
+    for r, c, v in zip(rows, cols, got):
+        w = (r % 1024) + 1024 * (c % 1024)
+        s = orc.skip(seeds[w], (r // 1024) * 64 + c // 1024)
+        assert v == orc.step(s) * 2.0 ** -31, (r, c)
+
+
+def skip_all(states, e):
+    """Every row of an (n, 6) state array advanced by 2^e steps (the oracle's
+    jump matrices T^(2^e), core.py:55-62, applied with exact uint64 sums)."""
+    j1, j2 = orc.jump_matrices(e)
+    out = np.empty_like(states)
+    for half, j, m in ((slice(0, 3), j1, sf.core.M1), (slice(3, 6), j2, sf.core.M2)):
+        v = states[:, half].astype(np.uint64)
+        acc = np.zeros_like(v)
+        for k in range(3):  # three products < 2^62 each: the sum fits uint64
+            acc += v[:, k:k + 1] * j.astype(np.uint64)[:, k][None, :]
+        out[:, half] = (acc % np.uint64(m)).astype(np.int64)
+    return out
+
+
+@pytest.mark.slow
+def test_normal_configs1_full_shape_vs_oracle():
+    """configs[1] at its real shape: 31250 x 32000 float32 normals from 2^18
+    streams on WorkGrid(512, 512) (ragged ownership: 31250 = 512*61 + 18 rows,
+    62.5 columns per lane) vs float32(oracle): <= 1 ulp_f32 everywhere,
+    identical on >= 99.999 % of the 1e9 cells, final states bit-exact."""
+    shape, g, n = (31250, 32000), (512, 512), 1 << 18
+    st = fresh(n)
+    got = sf.fill_normal(st, sf.FillRequest(shape=shape, grid=sf.WorkGrid(*g),
+                                            dtype=np.float32)).values
+    ref_st = oa.fresh_states(n)
+    ref = np.zeros(shape, np.float32)
+    orc.fill_normal(ref_st, ref.ravel(), shape[0], shape[1], shape[1], g[0], g[1])
+    assert np.array_equal(st.current, ref_st)
+    diff = got != ref
+    nd = int(diff.sum())
+    print(f"configs[1]: {nd} of {got.size} cells differ from float32(reference)")
+    assert nd <= got.size * 1e-5
+    if nd:
+        a = got[diff].astype(np.float64)
+        b = ref[diff].astype(np.float64)
+        assert (np.abs(a - b) <= np.spacing(np.abs(ref[diff])).astype(np.float64)).all()
 
 
 def test_sharded_api_single_rank(A):
@@ -751,3 +803,139 @@ def test_concurrent_host_threads_match_serial(G):
         for x in th:
             x.join()
         assert out == serial
+
+
+# ------------------------------------------- Fisher drop-in edge cases (r2)
+def _random_table(rows, cols, lam, seed):
+    t = np.random.default_rng(seed).poisson(lam, (rows, cols)).astype(np.int64)
+    t[0, 0] += 1  # total >= 1
+    return t
+
+
+@pytest.mark.parametrize("shape,lam", [((2, 300), 3.0), ((3, 500), 2.0), ((300, 2), 3.0)])
+def test_fisher_wide_tables_vs_oracle(shape, lam):
+    """Tables wider than the shared-memory column work (>~198 columns) run
+    with the column work in global memory (the reference allocates jwork for
+    any nc, _kernels.py:193-194): counts, statistics, states bit-exact."""
+    t = _random_table(*shape, lam, seed=shape[1])
+    st = fresh(64)
+    r = sf.fisher_sim(t, 640, st, grid=grid((8, 8)), return_stats=True)
+    ref_st = oa.fresh_states(64)
+    ref = oa.fisher(t, 640, ref_st, (8, 8), return_stats=True)
+    assert r.counts == ref["counts"] and r.sim_num == ref["sim_num"]
+    assert np.array_equal(r.statistics, ref["statistics"])
+    assert np.array_equal(st.current, ref_st)
+
+
+def test_fisher_wide_table_many_chunks():
+    """A wide table on a small grid: many replicate chunks visited grid-stride
+    by a capped grid; per-item counts and states bit-exact."""
+    t = _random_table(3, 500, 2.0, seed=7)
+    st = fresh(4)
+    r = sf.fisher_sim(t, 4 * 700, st, grid=grid((2, 2)), return_stats=True)
+    ref_st = oa.fresh_states(4)
+    ref = oa.fisher(t, 4 * 700, ref_st, (2, 2), return_stats=True)
+    assert r.counts == ref["counts"]
+    assert np.array_equal(r.statistics, ref["statistics"])
+    assert np.array_equal(st.current, ref_st)
+
+
+def test_rcont2_very_wide_table_uses_global_column_work():
+    """rcont2 on 2 x 20000 (80 KB of column work, beyond 48 KB of shared
+    memory): table and state equal the oracle's rcont2_table."""
+    rows = np.array([15000, 14000], np.int64)
+    cols = np.full(20000, 1, np.int64)
+    cols[:9000] += 1
+    lf = oa.lf_table(int(rows.sum()))
+    s_gpu = np.array([12345] * 6, np.int64)
+    s_ref = s_gpu.copy()
+    tab = sf.rcont2(rows, cols, s_gpu, lf)
+    ref = orc.rcont2_table(rows, cols, lf, s_ref)
+    assert np.array_equal(tab, ref)
+    assert np.array_equal(s_gpu, s_ref)
+
+
+def test_fisher_count_beyond_int32_per_cta():
+    """2^32 replicates on a one-item grid: one CTA counts ~2.9e9 hits, which
+    must not wrap (the reference counts in int64, _kernels.py:185,195,279).
+    Both possible 2x2 tables of these margins score 0 <= threshold, so every
+    replicate is a hit."""
+    st = fresh(1)
+    before = st.copy()
+    r = sf.fisher_sim([[1, 0], [0, 1]], 2 ** 32, st, grid=grid((1, 1)))
+    assert r.sim_num == 2 ** 32
+    assert r.counts == r.sim_num
+    s = sf.skip_ahead(before[0], 2 ** 32)  # one draw per replicate
+    assert st[0].g1 == s.g1 and st[0].g2 == s.g2
+
+
+# ------------------------------------------- host-path semantics (ADVICE r1)
+def test_held_current_reference_after_fisher_sim():
+    """A reference to `.current` held across fisher_sim calls behaves like the
+    reference's plain attribute: it shows the final states, and in-place edits
+    made through it are honoured by the next call."""
+    t4 = [[5, 9, 5, 7], [9, 5, 9, 7], [8, 6, 2, 6], [10, 8, 8, 8]]
+    st = fresh(2048)  # 96 KiB: the page-locked path
+    held = st.current
+    sf.fisher_sim(t4, 2048 * 3, st, grid=grid((32, 64)))
+    ref = oa.fresh_states(2048)
+    ref_ct = oa.fisher(t4, 2048 * 3, ref, (32, 64))
+    assert np.array_equal(held, ref)
+    held[:] = oa.fresh_states(2048)  # rewind in place through the held array
+    r = sf.fisher_sim(t4, 2048 * 3, st, grid=grid((32, 64)))
+    assert r.counts == ref_ct["counts"]
+    assert np.array_equal(held, ref)
+
+
+def test_held_current_reference_after_fill_refreshes_on_read():
+    """Fills leave the new states on the device (lazy host sync); the held
+    array is the same object and is refreshed in place at the next `.current`
+    read (documented contract)."""
+    st = fresh(2048)
+    held = st.current
+    sf.fill_uniform(st, sf.FillRequest(shape=(64, 128), grid=grid((32, 64))))
+    ref = oa.fresh_states(2048)
+    oa.fill("uniform", ref, (64, 128), (32, 64))
+    cur = st.current
+    assert cur is held
+    assert np.array_equal(held, ref)
+
+
+def test_shared_pinned_array_leaves_no_cuda_error():
+    """A StreamSet built on another one's (page-locked) array does not
+    register it twice, and no CUDA error is left behind for the next launch."""
+    import torch
+
+    a = fresh(4096)
+    a.device_current()  # page-locks a's array
+    b = sf.StreamSet(a.current, a.initial)
+    b.device_current()
+    x = torch.ones(1024, device="cuda") * 2  # a plain torch launch after the registrations
+    torch.cuda.synchronize()
+    assert float(x.sum()) == 2048.0
+    sf.fill_uniform(b, sf.FillRequest(shape=(8, 4096), grid=grid((1, 4096))))
+    ref = oa.fresh_states(4096)
+    oa.fill("uniform", ref, (8, 4096), (1, 4096))
+    assert np.array_equal(b.current, ref)
+
+
+def test_fisher_cache_on_two_streams_alternating_tables():
+    """Alternating tables on two CUDA streams: every call reuses or refills an
+    entry of the per-device input LRU; a reuse waits for the upload issued on
+    the other stream, an overwrite waits for readers on every stream."""
+    import torch
+
+    tabs = [np.array([[5, 9, 5, 7], [9, 5, 9, 7], [8, 6, 2, 6], [10, 8, 8, 8]]),
+            np.array([[3, 7], [6, 2]]), np.array([[5, 0, 4], [2, 6, 1]]),
+            np.array([[1, 2, 3, 4, 5], [5, 4, 3, 2, 1]]), np.array([[9, 1], [1, 9], [4, 4]]),
+            np.array([[2, 2, 2], [3, 3, 3], [1, 0, 7]])]
+    want = []
+    for t in tabs:
+        ref = oa.fresh_states(256)
+        want.append(oa.fisher(t, 256 * 40, ref, (16, 16))["counts"])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for rnd in range(3):
+        for k, t in enumerate(tabs):
+            with torch.cuda.stream(s1 if (k + rnd) % 2 else s2):
+                r = sf.fisher_sim(t, 256 * 40, fresh(256), grid=grid((16, 16)))
+            assert r.counts == want[k], (rnd, k)

@@ -540,3 +540,30 @@ def test_status_codes_match_header():
             assert type(exc).__name__ in comment, (name, type(exc))
             assert isinstance(exc, errors.StreamforgeError) and exc.status == int(code)
     assert type(errors.from_status(-12345, "x")) is errors.DeviceError
+
+
+def test_fill_dtype_validation_before_any_launch():
+    """run_grid_sharded validates kind/dtype like run_grid
+    (grid.py:112-123 order, then the dtype of the kind), and the C-ABI seam
+    refuses a buffer whose element size the kernel would overrun."""
+    import torch
+
+    from paper_2201_06604_b200.grid import launch_fill
+    from paper_2201_06604_b200.sharding import run_grid_sharded
+
+    st = sf.create_streams(sf.set_base_creator(), 16)[0]
+    g = sf.WorkGrid(4, 4)
+    for kind, dt in [("uniform", np.float32), ("exponential", np.float32),
+                     ("uniform-integer", np.float64), ("normal", np.int64),
+                     ("uniform", np.int64)]:
+        with pytest.raises(InvalidArgumentError):
+            run_grid_sharded(st, g, 8, 8, kind, dtype=dt, executor=object())
+        with pytest.raises(InvalidArgumentError):
+            sf.run_grid(st, g, 8, 8, kind, dtype=dt)
+    with pytest.raises(InvalidArgumentError):
+        run_grid_sharded(st, g, 8, 8, "poisson", executor=object())
+    cur = torch.zeros((16, 6), dtype=torch.int64)
+    for kind, tdt in [("uniform", torch.float32), ("exponential", torch.float32),
+                      ("uniform-integer", torch.float64), ("normal", torch.int64)]:
+        with pytest.raises(InvalidArgumentError):
+            launch_fill(kind, cur, 16, torch.empty((8, 8), dtype=tdt), 8, 8, 8, 4, 4)
