@@ -67,7 +67,7 @@ struct FisherArgs {
     int64_t item_lo, nloc, reps, rpc, nunits;
     int nr, nc, ntot, lf_len;
     MemoSet memo;  // memoised walks (memo.on)
-    // the memo's cell descriptors (row | col | box, 16-byte aligned,
+    // the memo's cell descriptors (fam | box, 16-byte aligned,
     // memo_bytes long) are staged into shared memory; the records stay in
     // global memory (L1/L2)
     const unsigned char *memo_blob;
@@ -86,7 +86,7 @@ using LfShared = LfPlain;
 
 // One unit = (item, replicate chunk): its replicates on the item's stream
 // from the chunk's start state; returns the unit's hits.
-template <int WALK, typename LF, typename JUMPS>
+template <int WALK, int NR, int NC, typename LF, typename JUMPS>
 __device__ __forceinline__ unsigned long long run_unit(const FisherArgs &a, const JUMPS &jumps,
                                                        int64_t u, const int32_t *rowm,
                                                        const int32_t *colm, const LF &lf,
@@ -102,8 +102,12 @@ __device__ __forceinline__ unsigned long long run_unit(const FisherArgs &a, cons
     Mrg s = load_state(a.cur + 6 * w);
     if (c) apply(jumps.j[c], s);
     for (int64_t rep = rep0; rep < rep1; ++rep) {
-        const double stat =
-            sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, lf, exptab, s, jw, js, nullptr, memo);
+        double stat;
+        if constexpr (NR > 0)  // compile-time shape: column work in registers
+            stat = sample_table_fixed<NR, NC, WALK>(rowm, colm, a.ntot, lf, exptab, s, memo);
+        else
+            stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, lf, exptab, s, jw, js,
+                                      nullptr, memo);
         if (stat <= a.threshold) ++uhits;  // _kernels.py:275-276
         if (a.stats) a.stats[local * a.reps + rep] = stat;
     }
@@ -118,7 +122,8 @@ __device__ __forceinline__ unsigned long long run_unit(const FisherArgs &a, cons
 // work and memo descriptors in global memory, units visited grid-stride (the
 // grid is sized to the global column-work allocation).  Hits are counted in
 // 64 bits end to end (the reference counts in int64, _kernels.py:185,195,279).
-template <bool LF_SMEM, int MINB, int WALK, typename JUMPS = ChunkJumps, bool WIDE = false>
+template <bool LF_SMEM, int MINB, int WALK, typename JUMPS = ChunkJumps, bool WIDE = false,
+          int NR = 0, int NC = 0>
 __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const FisherArgs a,
                                                          const __grid_constant__ JUMPS jumps) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         __syncthreads();
         const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t u = gtid; u < a.nunits; u += gstride)
-            hits += run_unit<WALK>(a, jumps, u, a.rowm, a.colm, LfGlobal{a.lf}, exptab,
+            hits += run_unit<WALK, 0, 0>(a, jumps, u, a.rowm, a.colm, LfGlobal{a.lf}, exptab,
                                    a.jwork_global + gtid, (int)a.jstride, a.memo);
     } else {
         const size_t off_row = 2048;
@@ -154,10 +159,8 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
             const uint4 *src = (const uint4 *)a.memo_blob;
             for (int t = threadIdx.x; t < (a.memo_bytes + 15) / 16; t += blockDim.x) dst[t] = src[t];
             const unsigned char *blob = a.memo_blob;
-            memo.row = (const MemoCellDesc *)(smem + off_memo +
-                                              ((const unsigned char *)a.memo.row - blob));
-            memo.col = (const MemoCellDesc *)(smem + off_memo +
-                                              ((const unsigned char *)a.memo.col - blob));
+            memo.fam = (const MemoCellDesc *)(smem + off_memo +
+                                              ((const unsigned char *)a.memo.fam - blob));
             if (a.memo.box)
                 memo.box = (const MemoBox *)(smem + off_memo +
                                              ((const unsigned char *)a.memo.box - blob));
@@ -166,10 +169,10 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         if (gtid < a.nunits) {  // one unit per thread
             int *jw = (int *)(smem + off_jw) + threadIdx.x;
             if (LF_SMEM)
-                hits = run_unit<WALK>(a, jumps, gtid, srow, scol, LfShared{lfs}, exptab, jw,
+                hits = run_unit<WALK, NR, NC>(a, jumps, gtid, srow, scol, LfShared{lfs}, exptab, jw,
                                       (int)blockDim.x, memo);
             else
-                hits = run_unit<WALK>(a, jumps, gtid, srow, scol, LfGlobal{a.lf}, exptab, jw,
+                hits = run_unit<WALK, NR, NC>(a, jumps, gtid, srow, scol, LfGlobal{a.lf}, exptab, jw,
                                       (int)blockDim.x, memo);
         }
     }
@@ -338,12 +341,10 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
                         const HostMemo *hm = nullptr, uint64_t memo_version = 0) {
     const size_t lf_off = align16((size_t)(nr + nc) * 4);
     const size_t key_bytes = lf_off + (size_t)lf_len * 8;
-    // [margins | lf] [row | col | box] [records]
-    size_t row_off = align16(key_bytes), col_off = row_off, box_off = row_off,
-           rec_off = row_off, bytes = key_bytes;
+    // [margins | lf] [fam | box] [records]
+    size_t row_off = align16(key_bytes), box_off = row_off, rec_off = row_off, bytes = key_bytes;
     if (hm) {
-        col_off = align16(row_off + hm->row.size() * sizeof(MemoCellDesc));
-        box_off = align16(col_off + hm->col.size() * sizeof(MemoCellDesc));
+        box_off = align16(row_off + hm->fam.size() * sizeof(MemoCellDesc));
         rec_off = align16(box_off + hm->box.size() * sizeof(MemoBox));
         rec_off = (rec_off + 127) & ~(size_t)127;  // records start on a 128-byte line
         bytes = rec_off + hm->rec.size() * 4;
@@ -398,8 +399,7 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
                     if (n) memcpy(en.pinned + off, src, n);
                 };
                 memset(en.pinned + key_bytes, 0, bytes - key_bytes);  // alignment gaps
-                put(row_off, hm->row.data(), hm->row.size() * sizeof(MemoCellDesc));
-                put(col_off, hm->col.data(), hm->col.size() * sizeof(MemoCellDesc));
+                put(row_off, hm->fam.data(), hm->fam.size() * sizeof(MemoCellDesc));
                 put(box_off, hm->box.data(), hm->box.size() * sizeof(MemoBox));
                 put(rec_off, hm->rec.data(), hm->rec.size() * 4);
             }
@@ -425,7 +425,6 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
     out.lf = (double *)(dev + lf_off);
     if (hm) {
         out.memo = MemoSet{(const MemoCellDesc *)(dev + row_off),
-                           (const MemoCellDesc *)(dev + col_off),
                            hm->box.empty() ? nullptr : (const MemoBox *)(dev + box_off),
                            (const uint32_t *)(dev + rec_off), hm->rec.empty() ? 0 : 1};
         out.memo_blob = dev + row_off;
@@ -506,42 +505,50 @@ static int sm_count() {  // of the current device, cached
     return n;
 }
 
-template <bool LF_SMEM, int MINB, int WALK>
-static cudaError_t launch_fisher_walk(unsigned blocks, size_t smem, cudaStream_t st,
-                                      const FisherArgs &a, const ChunkJumps &jumps) {
-    // raise the dynamic shared-memory limit once per instantiation and device
+// launch one fisher_kernel instantiation (the dynamic shared-memory limit is
+// raised once per instantiation and device)
+template <bool LF_SMEM, int MINB, int WALK, typename JUMPS, int NR = 0, int NC = 0>
+static cudaError_t launch_k(unsigned blocks, size_t smem, cudaStream_t st, const FisherArgs &a,
+                            const JUMPS &jumps) {
+    auto *k = fisher_kernel<LF_SMEM, MINB, WALK, JUMPS, false, NR, NC>;
     static std::atomic<uint64_t> done_mask{0};
     int d = 0;
     cudaGetDevice(&d);
     const uint64_t bit = 1ull << (d & 63);
     if (!(done_mask.load() & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(fisher_kernel<LF_SMEM, MINB, WALK>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kMaxFisherSmem);
+        cudaError_t e =
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxFisherSmem);
         if (e != cudaSuccess) return e;
         done_mask.fetch_or(bit);
     }
-    fisher_kernel<LF_SMEM, MINB, WALK><<<blocks, kFisherThreads, smem, st>>>(a, jumps);
+    k<<<blocks, kFisherThreads, smem, st>>>(a, jumps);
     return cudaGetLastError();
 }
 
-template <bool LF_SMEM, int MINB>
-static cudaError_t launch_fisher_large(unsigned blocks, size_t smem, cudaStream_t st,
-                                       const FisherArgs &a, const ChunkJumpsLarge &jumps) {
-    static std::atomic<uint64_t> done_mask{0};
-    int d = 0;
-    cudaGetDevice(&d);
-    const uint64_t bit = 1ull << (d & 63);
-    if (!(done_mask.load() & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(
-            fisher_kernel<LF_SMEM, MINB, kFisherWalkDefault, ChunkJumpsLarge>,
-            cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxFisherSmem);
-        if (e != cudaSuccess) return e;
-        done_mask.fetch_or(bit);
+// small tables with lf in shared memory: a compile-time shape when one of
+// these (the cell loops unroll, column work in registers); -1: none
+template <typename JUMPS>
+static int launch_fixed(int nr, int nc, unsigned blocks, size_t smem, cudaStream_t st,
+                        const FisherArgs &a, const JUMPS &j) {
+    constexpr int W = kFisherWalkDefault;
+    if (nr == 4 && nc == 4) {  // occupancy sweep (tuning)
+        switch (tune_knob("SFB_FISHER_FIXED_MINB", 4)) {
+            case 3: return launch_k<true, 3, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
+            case 5: return launch_k<true, 5, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
+            case 6: return launch_k<true, 6, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
+            default: break;
+        }
     }
-    fisher_kernel<LF_SMEM, MINB, kFisherWalkDefault, ChunkJumpsLarge>
-        <<<blocks, kFisherThreads, smem, st>>>(a, jumps);
-    return cudaGetLastError();
+    switch (nr * 16 + nc) {
+        case 0x22: return launch_k<true, 4, W, JUMPS, 2, 2>(blocks, smem, st, a, j);
+        case 0x23: return launch_k<true, 4, W, JUMPS, 2, 3>(blocks, smem, st, a, j);
+        case 0x32: return launch_k<true, 4, W, JUMPS, 3, 2>(blocks, smem, st, a, j);
+        case 0x33: return launch_k<true, 4, W, JUMPS, 3, 3>(blocks, smem, st, a, j);
+        case 0x34: return launch_k<true, 4, W, JUMPS, 3, 4>(blocks, smem, st, a, j);
+        case 0x43: return launch_k<true, 4, W, JUMPS, 4, 3>(blocks, smem, st, a, j);
+        case 0x44: return launch_k<true, 4, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
+        default: return -1;
+    }
 }
 
 // tables whose column work does not fit in shared memory (any width; the
@@ -557,10 +564,10 @@ template <bool LF_SMEM, int MINB>
 static cudaError_t launch_fisher(unsigned blocks, size_t smem, cudaStream_t st,
                                  const FisherArgs &a, const ChunkJumps &jumps) {
     switch (tune_knob("SFB_FISHER_WALK", kFisherWalkDefault)) {
-        case 0: return launch_fisher_walk<LF_SMEM, MINB, 0>(blocks, smem, st, a, jumps);
-        case 2: return launch_fisher_walk<LF_SMEM, MINB, 2>(blocks, smem, st, a, jumps);
-        case 1: return launch_fisher_walk<LF_SMEM, MINB, 1>(blocks, smem, st, a, jumps);
-        default: return launch_fisher_walk<LF_SMEM, MINB, 3>(blocks, smem, st, a, jumps);
+        case 0: return launch_k<LF_SMEM, MINB, 0>(blocks, smem, st, a, jumps);
+        case 2: return launch_k<LF_SMEM, MINB, 2>(blocks, smem, st, a, jumps);
+        case 1: return launch_k<LF_SMEM, MINB, 1>(blocks, smem, st, a, jumps);
+        default: return launch_k<LF_SMEM, MINB, 3>(blocks, smem, st, a, jumps);
     }
 }
 
@@ -716,13 +723,21 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     // register cap: 4 CTAs/SM (64 regs) -- best for every table measured on
     // B200 (tools/tune.py sweep of 3 walk forms x {3, 4} CTAs/SM)
     const int minb = tune_knob("SFB_FISHER_MINB", 4);
-    if (wide) {
+    const bool fixed_ok = lf_smem && minb >= 4 && tune_knob("SFB_FISHER_FIXED", 1) &&
+                          tune_knob("SFB_FISHER_WALK", kFisherWalkDefault) == kFisherWalkDefault;
+    int fx = -1;
+    if (!wide && fixed_ok)
+        fx = large ? launch_fixed(nr, nc, blocks, smem, st, a, jl)
+                   : launch_fixed(nr, nc, blocks, smem, st, a, jumps);
+    if (fx >= 0) {
+        e = (cudaError_t)fx;
+    } else if (wide) {
         e = launch_fisher_wide(blocks, smem, st, a, jl);
         cudaError_t ef = cudaFreeAsync(a.jwork_global, st);
         if (e == cudaSuccess) e = ef;
     } else if (large) {
-        e = lf_smem ? launch_fisher_large<true, 4>(blocks, smem, st, a, jl)
-                    : launch_fisher_large<false, 4>(blocks, smem, st, a, jl);
+        e = lf_smem ? launch_k<true, 4, kFisherWalkDefault>(blocks, smem, st, a, jl)
+                    : launch_k<false, 4, kFisherWalkDefault>(blocks, smem, st, a, jl);
     } else if (lf_smem) {
         if (minb >= 4)
             e = launch_fisher<true, 4>(blocks, smem, st, a, jumps);

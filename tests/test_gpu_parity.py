@@ -939,3 +939,22 @@ def test_fisher_cache_on_two_streams_alternating_tables():
             with torch.cuda.stream(s1 if (k + rnd) % 2 else s2):
                 r = sf.fisher_sim(t, 256 * 40, fresh(256), grid=grid((16, 16)))
             assert r.counts == want[k], (rnd, k)
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (2, 3), (3, 2), (3, 3), (3, 4), (4, 3), (4, 4)])
+@pytest.mark.parametrize("fixed", ["1", "0"])
+def test_fisher_fixed_shapes_vs_oracle(shape, fixed, monkeypatch):
+    """The compile-time-shape samplers (sample_table_fixed: unrolled cells,
+    column work in registers) and the generic one both equal the oracle:
+    counts, statistics and final states, on many chunks (small grid) and
+    with tabulated, truncated and walked configurations (lambda = 6 and 40)."""
+    monkeypatch.setenv("SFB_FISHER_FIXED", fixed)
+    for lam in (6.0, 40.0):
+        t = _random_table(*shape, lam, seed=shape[0] * 10 + shape[1])
+        st = fresh(16)
+        r = sf.fisher_sim(t, 16 * 300, st, grid=grid((4, 4)), return_stats=True)
+        ref_st = oa.fresh_states(16)
+        ref = oa.fisher(t, 16 * 300, ref_st, (4, 4), return_stats=True)
+        assert r.counts == ref["counts"]
+        assert np.array_equal(r.statistics, ref["statistics"])
+        assert np.array_equal(st.current, ref_st)
