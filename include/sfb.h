@@ -163,6 +163,18 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
                           int64_t item_lo, int64_t item_hi, double *d_stats,
                           int64_t *d_item_counts, uint64_t *d_count,
                           int zero_count, void *stream);
+/* Host-buffer form of sfb_fisher_replicates -- the call a host-authoritative
+ * fisher_sim makes (fisher.py:147-157: states, count and statistics in host
+ * memory; the reference's kernel call is synchronous): uploads rows
+ * [item_lo, item_hi) of h_cur (int64 (n_streams, 6), mutated in place), runs
+ * the kernels on `stream`, and returns after the final states, *h_count (=
+ * hits, not added) and h_stats (nullable; (w - item_lo)*reps + rep) are back
+ * in host memory.  Page-locked host arrays give direct DMA. */
+int sfb_fisher_replicates_host(int64_t *h_cur, int64_t n_streams, const int64_t *nrowt,
+                               int nr, const int64_t *ncolt, int nc, const double *lf,
+                               int64_t lf_len, double threshold, int64_t reps,
+                               int64_t item_lo, int64_t item_hi, double *h_stats,
+                               uint64_t *h_count, void *stream);
 /* _kernels.py:289-391 rcont2_table: one table from one 6-word state, run by
  * the same device sampler on one thread.  d_state: device int64[6] (mutated),
  * d_mat: device int64[nr*nc]. */

@@ -770,6 +770,77 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     return SFB_OK;
 }
 
+// Host-buffer form of sfb_fisher_replicates: the call a host-authoritative
+// fisher_sim makes (fisher.py:147-157 with states, count and statistics in
+// host memory).  Synchronous, like the reference's kernel call: uploads the
+// used rows [item_lo, item_hi) of the host state array into a per-device
+// scratch, runs the kernels, and copies the final states, the count and the
+// statistics (nullable) back before returning.  One mutex per device guards
+// the scratch for the whole call.
+struct HostCallScratch {
+    std::mutex mu;
+    unsigned char *dev = nullptr;
+    size_t cap = 0;
+};
+
+int sfb_fisher_replicates_host(int64_t *h_cur, int64_t n_streams, const int64_t *nrowt, int nr,
+                               const int64_t *ncolt, int nc, const double *lf, int64_t lf_len,
+                               double threshold, int64_t reps, int64_t item_lo, int64_t item_hi,
+                               double *h_stats, uint64_t *h_count, void *stream) {
+    if (!h_cur || !h_count) return fail(SFB_E_INVALID_ARGUMENT, "state and count buffers are required");
+    if (item_lo < 0 || item_hi < item_lo || item_hi > n_streams)
+        return fail(SFB_E_INSUFFICIENT_STREAMS, "item range [%lld, %lld) needs %lld streams, got %lld",
+                    (long long)item_lo, (long long)item_hi, (long long)item_hi,
+                    (long long)n_streams);
+    if (reps < 0) return fail(SFB_E_INVALID_ARGUMENT, "reps must be >= 0");
+    static HostCallScratch scratch[64];
+    int d = 0;
+    cudaGetDevice(&d);
+    HostCallScratch &sc = scratch[d & 63];
+    std::lock_guard<std::mutex> g(sc.mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nloc = item_hi - item_lo;
+    const size_t state_bytes = (size_t)nloc * 48;
+    const size_t stats_bytes = h_stats ? (size_t)nloc * (size_t)reps * 8 : 0;
+    const size_t need = 256 + ((state_bytes + 255) & ~(size_t)255) + stats_bytes;
+    cudaError_t e = cudaSuccess;
+    if (need > sc.cap) {
+        if (sc.dev) {
+            cudaStreamSynchronize(st);
+            cudaFree(sc.dev);
+        }
+        sc.dev = nullptr;
+        sc.cap = 0;
+        e = cudaMalloc((void **)&sc.dev, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SFB_E_CUDA, "fisher scratch allocation: %s", cudaGetErrorString(e));
+        }
+        sc.cap = need;
+    }
+    uint64_t *d_count = (uint64_t *)sc.dev;
+    int64_t *d_rows = (int64_t *)(sc.dev + 256);
+    double *d_stats = h_stats ? (double *)(sc.dev + 256 + ((state_bytes + 255) & ~(size_t)255))
+                              : nullptr;
+    if (nloc)
+        e = cudaMemcpyAsync(d_rows, h_cur + 6 * item_lo, state_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "state upload: %s", cudaGetErrorString(e));
+    // the kernel addresses stream w at cur + 6 w: rebase so row item_lo is d_rows[0]
+    if (int rc = sfb_fisher_replicates(d_rows - 6 * item_lo, n_streams, nrowt, nr, ncolt, nc, lf,
+                                       lf_len, threshold, reps, item_lo, item_hi, d_stats, nullptr,
+                                       d_count, 1, stream))
+        return rc;
+    if (nloc)
+        e = cudaMemcpyAsync(h_cur + 6 * item_lo, d_rows, state_bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && stats_bytes)
+        e = cudaMemcpyAsync(h_stats, d_stats, stats_bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h_count, d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher host call: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
 int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc, const double *lf,
                      int64_t lf_len, int64_t *d_state, int64_t *d_mat, void *stream) {
     int ntot = 0;
