@@ -166,20 +166,24 @@ def flush_l2(torch, scratch):
 
 # ------------------------------------------------------------------ workloads
 def run_uniform(torch, sf, rank, world, steps, warmup, cfg, kind="uniform"):
-    """C5: one fill of the full matrix per step, items sharded by columns."""
+    """C5: one fill of the full matrix per step, items sharded by grid columns;
+    each rank fills its compact shard (sharding.fill_shard_layout: ~1/N of
+    the matrix, the sub-grid fill on its offset stream block)."""
     from paper_2201_06604_b200.grid import launch_fill
+    from paper_2201_06604_b200.sharding import fill_shard_layout
 
     g0, g1 = cfg["g0"], cfg["g1"]
     st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
-    lo, hi = shard(g0 * g1, rank, world, align=4 * g0 if g1 % 4 == 0 else 2 * g0)
-    cur = st.device_current()
+    sh = fill_shard_layout(kind, cfg["nrow"], cfg["ncol"], g0, g1, rank, world)
+    lo, hi = sh.lo, sh.hi
+    cur = st.device_current()[lo:]
     dt = torch.int64 if kind == "uniform-integer" else torch.float64
-    out = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=dt, device="cuda")
+    out = torch.empty((sh.sub_nrow, sh.sub_ncol), dtype=dt, device="cuda")
     tm = Timer(torch)
 
     def step():
-        launch_fill(kind, cur, st.count, out, cfg["nrow"], cfg["ncol"], cfg["ncol"], g0, g1,
-                    item_lo=lo, item_hi=hi)
+        launch_fill(kind, cur, st.count - lo, out, sh.sub_nrow, sh.sub_ncol, sh.sub_ncol,
+                    sh.sub_g0, sh.sub_g1)
 
     for _ in range(warmup):
         step()
@@ -194,8 +198,7 @@ def run_uniform(torch, sf, rank, world, steps, warmup, cfg, kind="uniform"):
     values = cfg["nrow"] * cfg["ncol"]
     per_launch_ms = ms / steps
     # algorithmic bytes of this rank's launch: its output cells + state r/w
-    my_cells = values * (hi - lo) // (g0 * g1)
-    alg_bytes = my_cells * 8 + (hi - lo) * 48 * 2
+    alg_bytes = sh.cells * 8 + (hi - lo) * 48 * 2
     return dict(ms_per_step=ms / steps, value=values * steps / (ms / 1e3),
                 launch_ms=per_launch_ms, alg_bytes=alg_bytes, clocks=clk.summary(),
                 launches=steps, shard=[lo, hi])
@@ -219,17 +222,16 @@ def run_uniform_e2e(torch, sf, rank, world, steps, cfg):
             buf = sf.fill_uniform(st, req)
             buf.download(host)
     else:
-        from paper_2201_06604_b200.sharding import fill_shard, run_grid_sharded
+        from paper_2201_06604_b200.sharding import fill_shard_layout, run_grid_sharded
 
-        lo, hi = fill_shard("uniform", cfg["g0"], cfg["g1"], rank, world)
-        j_lo, j_hi = lo // cfg["g0"], hi // cfg["g0"]
-        host = torch.empty(cfg["nrow"] * (cfg["ncol"] // cfg["g1"]) * (j_hi - j_lo),
-                           dtype=torch.float64, pin_memory=True)
+        sh = fill_shard_layout("uniform", cfg["nrow"], cfg["ncol"], cfg["g0"], cfg["g1"], rank,
+                               world)
+        host = torch.empty((sh.sub_nrow, sh.sub_ncol), dtype=torch.float64, pin_memory=True)
 
         def step():
             _ = st.current
             buf = run_grid_sharded(st, g, cfg["nrow"], cfg["ncol"], "uniform")
-            buf.download_shard(cfg["g1"], j_lo, j_hi, host)
+            buf.download(host)  # the rank's compact shard: its cells only
     tm = Timer(torch)
     step()  # warm-up
     torch.cuda.synchronize()
@@ -250,17 +252,18 @@ def run_uniform_e2e(torch, sf, rank, world, steps, cfg):
 
 def run_normal(torch, sf, rank, world, steps, warmup, cfg, dtype):
     from paper_2201_06604_b200.grid import launch_fill
+    from paper_2201_06604_b200.sharding import fill_shard_layout
 
     g0, g1 = cfg["g0"], cfg["g1"]
     st = sf.create_streams(sf.set_base_creator(), cfg["n_streams"])[0]
-    lo, hi = shard(g0 * g1, rank, world, align=g1)
-    cur = st.device_current()
-    out = torch.empty((cfg["nrow"], cfg["ncol"]), dtype=dtype, device="cuda")
+    sh = fill_shard_layout("normal", cfg["nrow"], cfg["ncol"], g0, g1, rank, world)
+    cur = st.device_current()[sh.lo:]
+    out = torch.empty((sh.sub_nrow, sh.sub_ncol), dtype=dtype, device="cuda")
     tm = Timer(torch)
 
     def step():
-        launch_fill("normal", cur, st.count, out, cfg["nrow"], cfg["ncol"], cfg["ncol"], g0,
-                    g1, item_lo=lo, item_hi=hi)
+        launch_fill("normal", cur, st.count - sh.lo, out, sh.sub_nrow, sh.sub_ncol,
+                    sh.sub_ncol, sh.sub_g0, sh.sub_g1)
 
     for _ in range(warmup):
         step()

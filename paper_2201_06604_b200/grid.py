@@ -75,7 +75,22 @@ class MatrixBuffer:
         self.is_vector = is_vector
         self.dtype = np.dtype(dtype)
         self.tensor = tensor
+        self.shard = None  # sharded fills: the rank's FillShard (sharding.py)
         self._host = None if tensor is not None else np.zeros((nrow, npad), dtype=dtype)
+
+    @classmethod
+    def wrap(cls, tensor, dtype, ncol=None):
+        """A buffer around an existing (nrow, npad) CUDA tensor (sharded fills;
+        a rank whose streams own no cell gets an empty one)."""
+        obj = cls.__new__(cls)
+        obj.nrow, obj.npad = int(tensor.shape[0]), int(tensor.shape[1])
+        obj.ncol = obj.npad if ncol is None else ncol
+        obj.is_vector = False
+        obj.dtype = np.dtype(dtype)
+        obj.tensor = tensor
+        obj.shard = None
+        obj._host = None
+        return obj
 
     @classmethod
     def on_device(cls, nrow, ncol, npad=None, dtype=np.float64, is_vector=False, zero=False):

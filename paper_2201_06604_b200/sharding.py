@@ -3,13 +3,25 @@
 SURVEY.md §8(e): the stream index space shards naturally.  Rank g of G owns a
 contiguous block of stream ordinals:
   * uniform-kind fills (ordinal i + g0*j): a block of grid columns j, aligned
-    to column pairs so the 16-byte-store kernel applies;
+    to column quads / pairs so the wide-store kernels apply;
   * normal fills (ordinal i*g1 + j): a block of grid rows i;
   * fisher_sim: a block of work items (= streams).
-Fills need no data-path collective (each rank writes its cells; outputs stay
-sharded unless `gather=True`).  fisher_sim does ONE all-reduce of the int64 hit
-count.  Afterwards the updated stream states are all-gathered so every rank
-holds exactly the StreamSet a single-GPU run would have produced.
+
+Fills need no data-path collective and each rank allocates only its own
+cells.  A rank's block of grid columns [j_lo, j_hi) owns the matrix columns
+c = j + g1 q; stored compactly as (nrow, q, j) it is exactly the fill of a
+(nrow, Q w + rem) matrix on the sub-grid (g0, w = j_hi - j_lo) whose item
+(i, j') is stream i + g0 (j' + j_lo): the same kernel on the state array
+offset by g0 j_lo, the same draws in the same order (_kernels.py:50-80: an
+item visits its cells row-major).  Normal fills shard grid rows the same way
+(sub-grid (h, g1), stream offset i_lo g1, _kernels.py:108-166).  So per-rank
+memory is ~1/G of the matrix and the output can exceed one GPU's HBM;
+`gather_fill` assembles the full matrix on request.
+
+fisher_sim does ONE all-reduce of the int64 hit count.  Stream states: each
+rank advances only its block; with sync_states=True (default) the blocks are
+all-gathered so every rank holds exactly the StreamSet a single-GPU run would
+have produced (`sync_streams` does it later for callers that defer it).
 
 The per-shard work goes through an executor.  `DeviceExecutor` is the product
 (sm_100a kernels via the C ABI, NCCL over NVLink).  Tests substitute a CPU
@@ -18,6 +30,8 @@ GPUs; that executor lives in tests/ and is never used by the product path.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -45,6 +59,59 @@ def fill_shard(kind: str, g0: int, g1: int, rank: int, world: int):
     # whole column quads (the 256-bit store kernel) or pairs when possible
     align = 4 * g0 if g1 % 4 == 0 else 2 * g0 if g1 % 2 == 0 else g0
     return shard_range(g0 * g1, rank, world, align=align)
+
+
+@dataclass(frozen=True)
+class FillShard:
+    """One rank's block of a sharded fill and its compact layout.
+
+    Global problem: (nrow, ncol) on grid (g0, g1), stream ordinals [lo, hi).
+    Compact problem: (sub_nrow, sub_ncol) on grid (sub_g0, sub_g1), stream
+    ordinals [0, hi - lo) of the state array offset by `lo`."""
+
+    kind: str
+    nrow: int
+    ncol: int
+    g0: int
+    g1: int
+    lo: int
+    hi: int
+    sub_nrow: int
+    sub_ncol: int
+    sub_g0: int
+    sub_g1: int
+
+    @property
+    def cells(self) -> int:
+        return self.sub_nrow * self.sub_ncol
+
+    def global_index(self):
+        """Where the compact shard's rows (normal) or columns (uniform kinds)
+        sit in the global matrix: an int64 array over the sharded axis."""
+        if self.kind == "normal":
+            h, i_lo = max(self.sub_g0, 1), self.lo // self.g1
+            r = np.arange(self.sub_nrow, dtype=np.int64)
+            return i_lo + r % h + self.g0 * (r // h)
+        w, j_lo = max(self.sub_g1, 1), self.lo // self.g0
+        c = np.arange(self.sub_ncol, dtype=np.int64)
+        return j_lo + c % w + self.g1 * (c // w)
+
+
+def fill_shard_layout(kind: str, nrow: int, ncol: int, g0: int, g1: int, rank: int,
+                      world: int) -> FillShard:
+    """The compact layout of `rank`'s block (see the module docstring)."""
+    lo, hi = fill_shard(kind, g0, g1, rank, world)
+    if kind == "normal":
+        i_lo, i_hi = lo // g1, hi // g1
+        h = i_hi - i_lo
+        p, r0 = divmod(nrow, g0)
+        rows = p * h + min(max(r0 - i_lo, 0), h)
+        return FillShard(kind, nrow, ncol, g0, g1, lo, hi, rows, ncol if rows else 0, h, g1)
+    j_lo, j_hi = lo // g0, hi // g0
+    w = j_hi - j_lo
+    q, r0 = divmod(ncol, g1)
+    cols = q * w + min(max(r0 - j_lo, 0), w)
+    return FillShard(kind, nrow, ncol, g0, g1, lo, hi, nrow if cols else 0, cols, g0, w)
 
 
 def _dist():
@@ -86,11 +153,21 @@ class DeviceExecutor:
         self.commit_states(streams)
         return count, stats
 
-    def fill(self, kind, streams, nrow, ncol, npad, g0, g1, lo, hi, rate, dtype, zero):
+    def fill(self, shard: FillShard, streams, rate, dtype):
+        """The rank's compact shard: the sub-grid fill on the offset states."""
+        import torch
+
+        from .grid import _torch_dtype
+
         cur = self.states(streams)
-        buf = MatrixBuffer.on_device(nrow, ncol, npad, dtype=dtype, zero=zero)
-        launch_fill(kind, cur, streams.count, buf.tensor, nrow, ncol, buf.npad, g0, g1,
-                    rate=rate, item_lo=lo, item_hi=hi)
+        if shard.cells == 0:  # this rank's streams own no cell (and do not advance)
+            t = torch.empty((shard.sub_nrow, shard.sub_ncol), dtype=_torch_dtype(dtype),
+                            device=self.device)
+            return MatrixBuffer.wrap(t, dtype)
+        buf = MatrixBuffer.on_device(shard.sub_nrow, shard.sub_ncol, dtype=dtype)
+        launch_fill(shard.kind, cur[shard.lo:], streams.count - shard.lo, buf.tensor,
+                    shard.sub_nrow, shard.sub_ncol, shard.sub_ncol, shard.sub_g0, shard.sub_g1,
+                    rate=rate)
         self.commit_states(streams)
         return buf
 
@@ -117,8 +194,16 @@ def _allgather_rows(executor, streams, lo, hi, group):
     executor.commit_states(streams)
 
 
+def sync_streams(streams, lo, hi, group=None, executor=None):
+    """Collective: after sharded calls made with sync_states=False, every rank
+    contributes its block [lo, hi) and ends with the full single-GPU state."""
+    _, world = _world(group)
+    if world > 1:
+        _allgather_rows(executor or DeviceExecutor(), streams, lo, hi, group)
+
+
 def fisher_sim_sharded(table, n, streams, grid, return_stats=False, group=None,
-                       executor=None) -> FisherResult:
+                       executor=None, sync_states=True) -> FisherResult:
     """fisher_sim (fisher.py:118-164) over all ranks of `group`: identical
     counts, p-value, statistics and final states to a single-device run."""
     import torch
@@ -147,29 +232,62 @@ def fisher_sim_sharded(table, n, streams, grid, return_stats=False, group=None,
                 pieces.append(part[: (b - a) * plan.reps])
             stats = torch.cat(pieces)
         full_stats = _lib.to_host(stats)
-    if world > 1:
+    if world > 1 and sync_states:
         _allgather_rows(executor, streams, lo, hi, group)
     return FisherResult(threshold=plan.threshold, sim_num=plan.sim_num, counts=counts,
                         p_value=(1 + counts) / (plan.sim_num + 1), statistics=full_stats)
 
 
-def run_grid_sharded(streams, grid, nrow, ncol, kind, rate=1.0, npad=None, dtype=None,
-                     group=None, executor=None, gather=False):
-    """run_grid (grid.py:112-144) over all ranks: each rank fills the cells of
-    its stream block; states are all-gathered.  With gather=True the buffers
-    start zeroed and are summed across ranks (disjoint cells), so every rank
-    returns the full matrix; otherwise only the rank's own cells are valid."""
+def gather_fill(buf: MatrixBuffer, group=None, npad=None) -> MatrixBuffer:
+    """Collective: every rank's compact shard of one sharded fill, assembled
+    into the full (nrow, npad) matrix on every rank (an all-gather of the
+    shards padded to the largest; padding columns zero)."""
+    import torch
+
     dist = _dist()
+    shard = buf.shard
+    _, world = _world(group)
+    npad = shard.ncol if npad is None else npad
+    full = torch.zeros((shard.nrow, npad), dtype=buf.tensor.dtype, device=buf.tensor.device)
+    layouts = [fill_shard_layout(shard.kind, shard.nrow, shard.ncol, shard.g0, shard.g1, r,
+                                 world) for r in range(world)]
+    if world > 1:
+        width = max(max(s.cells for s in layouts), 1)
+        mine = torch.zeros(width, dtype=buf.tensor.dtype, device=buf.tensor.device)
+        mine[: shard.cells] = buf.tensor.reshape(-1)
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=group)
+    else:
+        parts = [buf.tensor.reshape(-1)]
+    for s, part in zip(layouts, parts):
+        if s.cells == 0:
+            continue
+        piece = part[: s.cells].reshape(s.sub_nrow, s.sub_ncol)
+        idx = torch.from_numpy(s.global_index()).to(full.device)
+        if s.kind == "normal":
+            full.index_copy_(0, idx, piece)
+        else:
+            full.index_copy_(1, idx, piece)
+    return MatrixBuffer.wrap(full, buf.dtype, ncol=shard.ncol)
+
+
+def run_grid_sharded(streams, grid, nrow, ncol, kind, rate=1.0, npad=None, dtype=None,
+                     group=None, executor=None, gather=False, sync_states=True):
+    """run_grid (grid.py:112-144) over all ranks: each rank fills the cells of
+    its stream block into a compact shard (`.shard` describes it; ~1/G of the
+    matrix per rank).  gather=True returns the full (nrow, npad) matrix on
+    every rank instead (gather_fill).  sync_states=True all-gathers the
+    advanced stream blocks so every rank ends with the single-GPU StreamSet."""
     out_dtype = check_fill(streams, grid, kind, dtype)
     executor = executor or DeviceExecutor()
     rank, world = _world(group)
-    lo, hi = fill_shard(kind, grid.nglobal0, grid.nglobal1, rank, world)
-    buf = executor.fill(kind, streams, nrow, ncol, ncol if npad is None else npad,
-                        grid.nglobal0, grid.nglobal1, lo, hi, rate, out_dtype,
-                        zero=gather and world > 1)
-    if world > 1:
-        if gather:
-            dist.all_reduce(buf.tensor, op=dist.ReduceOp.SUM, group=group)
-        _allgather_rows(executor, streams, lo, hi, group)
-    buf.shard = (lo, hi)
+    shard = fill_shard_layout(kind, nrow, ncol, grid.nglobal0, grid.nglobal1, rank, world)
+    buf = executor.fill(shard, streams, rate, out_dtype)
+    buf.shard = shard
+    if world > 1 and sync_states:
+        _allgather_rows(executor, streams, shard.lo, shard.hi, group)
+    if gather:
+        full = gather_fill(buf, group, npad=ncol if npad is None else npad)
+        full.shard = shard
+        return full
     return buf

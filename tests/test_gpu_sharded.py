@@ -47,8 +47,22 @@ def _worker(rank, world, port, outdir):
             st = sf.create_streams(sf.set_base_creator(), g[0] * g[1])[0]
             buf = sharding.run_grid_sharded(st, sf.WorkGrid(*g), shape[0], shape[1], kind,
                                             gather=True)
+            # the compact shard alone (what a rank keeps): its cells only
+            st2 = sf.create_streams(sf.set_base_creator(), g[0] * g[1])[0]
+            part = sharding.run_grid_sharded(st2, sf.WorkGrid(*g), shape[0], shape[1], kind)
             res[kind] = dict(data=buf.tensor.cpu().numpy().copy(), states=st.current.copy(),
-                             shard=buf.shard)
+                             shard=buf.shard, part=part.tensor.cpu().numpy().copy(),
+                             part_bytes=part.tensor.numel() * part.tensor.element_size(),
+                             states2=st2.current.copy())
+        # capacity: a C5-layout fill (2^14 streams, 2048 x 8192 f64 = 128 MiB)
+        # allocates ~1/world of it per rank
+        st = sf.create_streams(sf.set_base_creator(), 1 << 14)[0]
+        torch.cuda.synchronize()
+        before = torch.cuda.memory_allocated()
+        part = sharding.run_grid_sharded(st, sf.WorkGrid(128, 128), 2048, 8192, "uniform",
+                                         sync_states=False)
+        res["capacity"] = dict(bytes=torch.cuda.memory_allocated() - before,
+                               cells=part.shard.cells)
         with open(os.path.join(outdir, f"r{rank}.pkl"), "wb") as fh:
             pickle.dump(res, fh)
     finally:
@@ -82,8 +96,22 @@ def test_sharded_ranks_equal_single_device(world):
         fill = {"uniform": sf.fill_uniform, "normal": sf.fill_normal,
                 "exponential": sf.fill_exponential}[kind]
         want = fill(st, req).data
-        shards = {tuple(r[kind]["shard"]) for r in out}
+        shards = {r[kind]["shard"] for r in out}
         assert len(shards) == world, kind  # every rank owned a distinct block
+        cells = 0
         for r in out:
             assert np.array_equal(r[kind]["data"][:, :shape[1]], want), kind
             assert np.array_equal(r[kind]["states"], st.current), kind
+            assert np.array_equal(r[kind]["states2"], st.current), kind
+            sh = r[kind]["shard"]
+            idx = sh.global_index()
+            assert r[kind]["part"].shape == (sh.sub_nrow, sh.sub_ncol)
+            if sh.cells:
+                ref = want[idx, :] if kind == "normal" else want[:, idx]
+                assert np.array_equal(r[kind]["part"], ref), kind
+            cells += sh.cells
+        assert cells == shape[0] * shape[1], kind  # the shards tile the matrix
+    for r in out:
+        cap = r["capacity"]
+        assert cap["cells"] * 8 == 2048 * 8192 * 8 // world
+        assert cap["bytes"] <= 2048 * 8192 * 8 // world + (2 << 20)  # + allocator rounding

@@ -69,18 +69,20 @@ class OracleExecutor:
         st = torch.from_numpy(stats[lo * plan.reps:hi * plan.reps].copy()) if want_stats else None
         return torch.tensor([cnt], dtype=torch.int64), st
 
-    def fill(self, kind, streams, nrow, ncol, npad, g0, g1, lo, hi, rate, dtype, zero):
+    def fill(self, shard, streams, rate, dtype):
+        """The rank's compact shard, cut from a full oracle fill through the
+        shard's own index map (an independent check of the sub-grid claim)."""
         cur = streams._current
         work = cur.copy()
-        full = oa.fill(kind, work, (nrow, ncol), (g0, g1), npad=npad, rate=rate,
-                       out_dtype=dtype)
-        r = np.arange(nrow)[:, None] % g0
-        c = np.arange(npad)[None, :] % g1
-        owner = r * g1 + c if kind == "normal" else r + g0 * c
-        mine = (owner >= lo) & (owner < hi) & (np.arange(npad)[None, :] < ncol)
-        data = np.where(mine, full, np.zeros_like(full))
-        cur[lo:hi] = work[lo:hi]
-        return MatrixBuffer(nrow, ncol, npad, dtype, tensor=torch.from_numpy(data))
+        full = oa.fill(shard.kind, work, (shard.nrow, shard.ncol), (shard.g0, shard.g1),
+                       rate=rate, out_dtype=dtype)
+        idx = shard.global_index()
+        if shard.kind == "normal":
+            piece = full[idx, :][:, : shard.sub_ncol] if shard.cells else full[:0, :0]
+        else:
+            piece = full[:, idx][: shard.sub_nrow] if shard.cells else full[:0, :0]
+        cur[shard.lo:shard.hi] = work[shard.lo:shard.hi]
+        return MatrixBuffer.wrap(torch.from_numpy(np.ascontiguousarray(piece)), dtype)
 
 
 # -------------------------------------------------------------- workers
@@ -110,7 +112,12 @@ def _worker(rank, world, port, job, outdir):
             st = sf.create_streams(sf.set_base_creator(), g[0] * g[1])[0]
             buf = sharding.run_grid_sharded(st, sf.WorkGrid(*g), shape[0], shape[1], kind,
                                             executor=ex, gather=True)
-            res = dict(data=buf.data.copy(), states=st.current.copy(), shard=buf.shard)
+            st2 = sf.create_streams(sf.set_base_creator(), g[0] * g[1])[0]
+            part = sharding.run_grid_sharded(st2, sf.WorkGrid(*g), shape[0], shape[1], kind,
+                                             executor=ex)
+            res = dict(data=buf.data.copy(), states=st.current.copy(), shard=buf.shard,
+                       part=part.tensor.numpy().copy(), part_shard=part.shard,
+                       states2=st2.current.copy())
         with open(os.path.join(outdir, f"r{rank}.pkl"), "wb") as fh:
             pickle.dump(res, fh)
     finally:
@@ -149,6 +156,43 @@ def test_fill_sharded_equals_single_device(job):
     ref_st = oa.fresh_states(g[0] * g[1])
     ref = oa.fill(kind, ref_st, shape, g)
     assert out[0]["shard"] != out[1]["shard"]
+    cells = 0
     for r in out:
         assert np.array_equal(r["data"], ref)
         assert np.array_equal(r["states"], ref_st)
+        assert np.array_equal(r["states2"], ref_st)
+        # the compact shard: exactly the rank's cells, nothing else allocated
+        sh = r["part_shard"]
+        idx = sh.global_index()
+        assert r["part"].shape == (sh.sub_nrow, sh.sub_ncol)
+        if sh.cells:  # a rank whose block owns no cell holds an empty shard
+            want = ref[idx, :] if kind == "normal" else ref[:, idx]
+            assert np.array_equal(r["part"], want)
+        cells += r["part"].size
+    assert cells == shape[0] * shape[1]
+
+
+@pytest.mark.parametrize("kind", ["uniform", "normal"])
+def test_fill_shard_layout_tiles_the_matrix(kind):
+    """Every (shape, grid, world): the compact shards' index maps partition
+    the sharded axis, and each shard is the sub-grid fill on offset states
+    (checked on the oracle: sub-problem == the rank's cells of the whole)."""
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        g0, g1 = int(rng.integers(1, 7)), 2 * int(rng.integers(1, 5))
+        nrow, ncol = int(rng.integers(1, 30)), int(rng.integers(1, 30))
+        world = int(rng.integers(1, 5))
+        ref_st = oa.fresh_states(g0 * g1)
+        ref = oa.fill(kind, ref_st.copy(), (nrow, ncol), (g0, g1))
+        seen = []
+        for r in range(world):
+            sh = sharding.fill_shard_layout(kind, nrow, ncol, g0, g1, r, world)
+            seen.extend(sh.global_index().tolist() if sh.cells else [])
+            if not sh.cells:
+                continue
+            st = oa.fresh_states(g0 * g1)[sh.lo:].copy()
+            sub = oa.fill(kind, st, (sh.sub_nrow, sh.sub_ncol), (sh.sub_g0, sh.sub_g1))
+            idx = sh.global_index()
+            want = ref[idx, :] if kind == "normal" else ref[:, idx]
+            assert np.array_equal(sub, want), (g0, g1, nrow, ncol, world, r)
+        assert sorted(seen) == list(range(nrow if kind == "normal" else ncol))
