@@ -72,6 +72,7 @@ struct FisherArgs {
     // global memory (L1/L2)
     const unsigned char *memo_blob;
     int memo_bytes;  // > 0: stage into shared memory
+    int64_t rec_bytes;  // memo records (L2 prefetch at kernel start)
     // WIDE launches (column work too large for shared memory): per-thread
     // column work in global memory, jw[m * jstride + thread]
     int *jwork_global;
@@ -152,6 +153,21 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         for (int t = threadIdx.x; t < a.nc; t += blockDim.x) scol[t] = a.colm[t];
         if (LF_SMEM)
             for (int t = threadIdx.x; t < a.lf_len; t += blockDim.x) lfs[t] = a.lf[t];
+        // the memo records: this CTA's slice prefetched into L2 (the first
+        // touches of a cold table would otherwise be DRAM round trips on the
+        // lookups' critical path)
+        if (a.rec_bytes > 0 && threadIdx.x == 0) {
+            const int64_t slice = ((a.rec_bytes + gridDim.x - 1) / gridDim.x + 127) & ~(int64_t)127;
+            const int64_t off = slice * blockIdx.x;
+            if (off < a.rec_bytes) {
+                const uint32_t len = (uint32_t)min(slice, a.rec_bytes - off) & ~15u;
+                if (len)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     (const unsigned char *)a.memo.rec + off),
+                                 "r"(len)
+                                 : "memory");
+            }
+        }
         // the memo's cell descriptors: one cooperative copy, pointers rebased
         MemoSet memo = a.memo;
         if (memo.on) {
@@ -297,6 +313,7 @@ struct StagedInputs {
     MemoSet memo{};
     const unsigned char *memo_blob = nullptr;
     size_t memo_bytes = 0;
+    size_t rec_bytes = 0;
     // record the consumer kernel (call after the launch, lock still held)
     void done(cudaStream_t st) {
         for (auto &r : entry->readers)
@@ -429,6 +446,7 @@ static int stage_inputs(const int64_t *nrowt, int nr, const int64_t *ncolt, int 
                            (const uint32_t *)(dev + rec_off), hm->rec.empty() ? 0 : 1};
         out.memo_blob = dev + row_off;
         out.memo_bytes = rec_off - row_off;  // the descriptors (staged per CTA)
+        out.rec_bytes = hm->rec.size() * 4;
     }
     return SFB_OK;
 }
@@ -531,14 +549,6 @@ template <typename JUMPS>
 static int launch_fixed(int nr, int nc, unsigned blocks, size_t smem, cudaStream_t st,
                         const FisherArgs &a, const JUMPS &j) {
     constexpr int W = kFisherWalkDefault;
-    if (nr == 4 && nc == 4) {  // occupancy sweep (tuning)
-        switch (tune_knob("SFB_FISHER_FIXED_MINB", 4)) {
-            case 3: return launch_k<true, 3, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
-            case 5: return launch_k<true, 5, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
-            case 6: return launch_k<true, 6, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
-            default: break;
-        }
-    }
     switch (nr * 16 + nc) {
         case 0x22: return launch_k<true, 4, W, JUMPS, 2, 2>(blocks, smem, st, a, j);
         case 0x23: return launch_k<true, 4, W, JUMPS, 2, 3>(blocks, smem, st, a, j);
@@ -685,6 +695,7 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     if (!use_memo) a.memo = MemoSet{};
     a.memo_blob = in.memo_blob;
     a.memo_bytes = use_memo ? (int)in.memo_bytes : 0;
+    a.rec_bytes = use_memo && tune_knob("SFB_FISHER_PREFETCH", 1) ? (int64_t)in.rec_bytes : 0;
 
     // shared memory layout of fisher_kernel (same offsets): exp table |
     // margins | [lf] | column work | memo cell descriptors; lf goes to global

@@ -942,19 +942,20 @@ def test_fisher_cache_on_two_streams_alternating_tables():
 
 
 @pytest.mark.parametrize("shape", [(2, 2), (2, 3), (3, 2), (3, 3), (3, 4), (4, 3), (4, 4)])
-@pytest.mark.parametrize("fixed", ["1", "0"])
-def test_fisher_fixed_shapes_vs_oracle(shape, fixed, monkeypatch):
+@pytest.mark.parametrize("mode", ["fixed", "generic"])
+def test_fisher_fixed_shapes_vs_oracle(shape, mode, monkeypatch):
     """The compile-time-shape samplers (sample_table_fixed: unrolled cells,
     column work in registers) and the generic one both equal the oracle:
-    counts, statistics and final states, on many chunks (small grid) and
-    with tabulated, truncated and walked configurations (lambda = 6 and 40)."""
-    monkeypatch.setenv("SFB_FISHER_FIXED", fixed)
-    for lam in (6.0, 40.0):
+    counts, statistics and final states, on many chunks (small grid), odd
+    and even replicate counts, with tabulated, truncated and walked
+    configurations (lambda = 6 and 40)."""
+    monkeypatch.setenv("SFB_FISHER_FIXED", "0" if mode == "generic" else "1")
+    for lam, n in ((6.0, 16 * 300), (40.0, 16 * 301), (6.0, 16 * 7)):
         t = _random_table(*shape, lam, seed=shape[0] * 10 + shape[1])
         st = fresh(16)
-        r = sf.fisher_sim(t, 16 * 300, st, grid=grid((4, 4)), return_stats=True)
+        r = sf.fisher_sim(t, n, st, grid=grid((4, 4)), return_stats=True)
         ref_st = oa.fresh_states(16)
-        ref = oa.fisher(t, 16 * 300, ref_st, (4, 4), return_stats=True)
+        ref = oa.fisher(t, n, ref_st, (4, 4), return_stats=True)
         assert r.counts == ref["counts"]
         assert np.array_equal(r.statistics, ref["statistics"])
         assert np.array_equal(st.current, ref_st)
