@@ -15,7 +15,8 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsfb.so")
+# SFB_LIB: load another build of the library (A/B timing of kernel changes only)
+LIB_PATH = os.environ.get("SFB_LIB") or os.path.join(_HERE, "libsfb.so")
 
 SFB_F64, SFB_F32, SFB_I64 = 0, 1, 2
 

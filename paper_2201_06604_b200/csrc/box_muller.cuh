@@ -42,7 +42,8 @@ namespace sfb {
 enum BmCoef {
     kC_Ln2Hi, kC_Ln2Lo, kC_L5, kC_L4, kC_L3, kC_L2,  // ln(1+r) coefficients 1/5, -1/4, 1/3, -1/2
     kC_S5, kC_S3, kC_C4, kC_C2,                      // sin B, cos B - 1
-    kC_TwoPiNorm, kC_HalfPi, kC_PiO2Lo, kC_Neg2, kC_Ln2, kC_Half, kC_Count
+    kC_TwoPiNorm, kC_HalfPi, kC_PiO2Lo, kC_Neg2, kC_Ln2, kC_Half, kC_3o8, kC_Neg2Ln2,
+    kC_TwoPiNormBias, kC_M2L5, kC_M2L4, kC_M2L3, kC_One, kC_Count
 };
 
 #define SFB_BM_COEF_INIT                                                                 \
@@ -53,7 +54,10 @@ enum BmCoef {
             1.0 / 24.0, -1.0 / 2.0, (2.0 * 3.141592653589793) / 2147483648.0,            \
             0.5 * 3.141592653589793, /* HALFPI, _kernels.py:22 */                         \
             6.123233995736766e-17,   /* pi/2 - HALFPI */                                  \
-            -2.0, 6.93147180559945286227e-01, /* ln 2 rounded */ 0.5                     \
+            -2.0, 6.93147180559945286227e-01, /* ln 2 rounded */ 0.5,                    \
+            0.375, -1.38629436111989057245, /* -2 ln 2 rounded */                          \
+            (2.0 * 3.141592653589793) * -2097152.0, /* -2^52 TWOPI 2^-31 (exact) */      \
+            -2.0 / 5.0, 2.0 / 4.0, -2.0 / 3.0, 1.0                                         \
     }
 
 #ifdef __CUDACC__
@@ -156,13 +160,17 @@ SFB_EXP_HD void box_muller_pair(uint32_t z1m1, uint32_t z2m1, const uint64_t *lo
 // far below 2^-24, not the ~2^-52 of box_muller_pair: this form targets
 // <= 2^-44, so a result can differ from float32(reference) only when the
 // reference lies within ~2^-44 of a float32 rounding boundary (expected rate
-// ~1e-6 of cells, by 1 ulp_f32).  FP64 work drops from ~45 to ~25 ops/pair:
-//   * log: k ln2 + ln c in one fma against a table of (1/c, ln c rounded)
-//     pairs (one 16-byte load), degree-5 polynomial kept (|r| <= 2^-10 and
-//     ln u1 ~ r near u1 = 1, where r^5/5 is 2^-42 relative);
-//   * sqrt: rsqrt.approx seed (MUFU.RSQ64H, measured <= 2^-20.06 relative on
-//     B200), one Newton step on 1/sqrt and one residual-corrected step on
-//     sqrt (NEWTON = 2; error ~(1.5 e^2)^2, far below 2^-53);
+// ~1e-6 of cells, by 1 ulp_f32).  FP64 work drops from ~45 to ~23 ops/pair:
+//   * log: x = -2 ln u1 directly: the table holds (1/c, -2 ln c) (one
+//     16-byte load), -2 k ln2 + (-2 ln c) in one fma, and -2 ln(1+r) as
+//     -2r + r^2 q(r) with the degree-5 coefficients pre-scaled by -2 (the
+//     scaling commutes with every rounding), so no separate -2 multiply;
+//     |r| <= 2^-10 and ln u1 ~ r near u1 = 1, where r^5/5 is 2^-42 relative;
+//   * sqrt: rsqrt.approx seed y0 (MUFU.RSQ64H, measured <= 2^-20.06 relative
+//     on B200), e = 1 - x y0^2, R = x y0 (1 + e/2 + 3e^2/8): 6 FP64 ops,
+//     truncation 5e^3/16 < 2^-58;
+//   * theta: fma(2^52 + z2, c, -2^52 c) = fl(c z2) from the integer bits
+//     (no I2F on the XU pipe);
 //   * trig: sin B to B^3 (B^5/120 < 2.3e-15 absolute), cos B - 1 to B^4,
 //     fused fma recombination; (cos A, sin A) as one 16-byte load;
 //   * lane b = R sin(theta): the reference's cos(fl(theta - fl(pi/2))) differs
@@ -175,14 +183,17 @@ SFB_EXP_HD void box_muller_pair(uint32_t z1m1, uint32_t z2m1, const uint64_t *lo
 struct alignas(16) BmPair {
     double x, y;
 };
-constexpr int kBmFastLogPairs = SFB_BM_LOG_N;         // (1/c, ln c)
+constexpr int kBmFastLogPairs = SFB_BM_LOG_N;         // (1/c, -2 ln c)
 constexpr int kBmFastTrigPairs = SFB_BM_TRIG_N + 1;   // (cos A, sin A)
 
 // fill the fast-path tables from the table words of bm_tables.inc
+constexpr double kBmF32LogScale = -2.0;  // logp[i].y = -2 ln c (box_muller_pair_f32_core)
 SFB_EXP_HD void bm_fast_tables(const uint64_t *logw, const uint64_t *trigw, int t, int nt,
-                               BmPair *logp, BmPair *trigp, double *angle) {
+                               BmPair *logp, BmPair *trigp, double *angle,
+                               double yscale = kBmF32LogScale) {
     for (int i = t; i < kBmFastLogPairs; i += nt)
-        logp[i] = BmPair{as_f64(logw[3 * i]), as_f64(logw[3 * i + 1]) + as_f64(logw[3 * i + 2])};
+        logp[i] = BmPair{as_f64(logw[3 * i]),
+                         (as_f64(logw[3 * i + 1]) + as_f64(logw[3 * i + 2])) * yscale};
     for (int i = t; i < kBmFastTrigPairs; i += nt) {
         trigp[i] = BmPair{as_f64(trigw[3 * i + 1]), as_f64(trigw[3 * i + 2])};
         angle[i] = as_f64(trigw[3 * i]);
@@ -234,8 +245,9 @@ SFB_EXP_HD bool bm_f32_needs_exact(uint32_t z2m1) {
 
 // the fast form without the exact fallback (callers test bm_f32_needs_exact;
 // keeping the rare branch out of this function lets the compiler interleave
-// several pairs in one basic block)
-template <int NEWTON, typename SEED = RsqrtSeedHw>
+// several pairs in one basic block).  logp[i] = (1/c, -2 ln c) as staged by
+// bm_fast_tables(..., kBmF32LogScale).
+template <typename SEED = RsqrtSeedHw>
 SFB_EXP_HD void box_muller_pair_f32_core(uint32_t z1m1, uint32_t z2m1, const BmPair *logp,
                                          const BmPair *trigp, const double *angle, float &a,
                                          float &b, const SEED &seed = SEED()) {
@@ -245,22 +257,24 @@ SFB_EXP_HD void box_muller_pair_f32_core(uint32_t z1m1, uint32_t z2m1, const BmP
     const double m = as_f64((bits & 0x000fffffffffffffull) | 0x3fe0000000000000ull);
     const BmPair lc = logp[(uint32_t)(bits >> 43) & (SFB_BM_LOG_N - 1)];
     const double r = fma_rn(m, lc.x, -1.0);
-    double p = fma_rn(r, SFB_BMC(kC_L5), SFB_BMC(kC_L4));
-    p = fma_rn(r, p, SFB_BMC(kC_L3));
-    p = fma_rn(r, p, SFB_BMC(kC_L2));
+    // x = -2 ln u1 = (-2 k ln2 - 2 ln c) - 2r + r^2 (1 + r (-2/3 + r (1/2 - 2r/5))):
+    // -2 ln(1+r) with the -2 folded into the table and the coefficients
+    double p = fma_rn(r, SFB_BMC(kC_M2L5), SFB_BMC(kC_M2L4));
+    p = fma_rn(r, p, SFB_BMC(kC_M2L3));
+    p = fma_rn(r, p, SFB_BMC(kC_One));
     const double r2 = r * r;
-    const double y = fma_rn((double)k, SFB_BMC(kC_Ln2), lc.y);
-    const double x = SFB_BMC(kC_Neg2) * (y + fma_rn(r2, p, r));  // -2 ln u1 (scaling exact)
-    double yr = seed(x);
-    if (NEWTON >= 2) {  // y <- y + y/2 (1 - x y^2)
-        const double e = fma_rn(-x, yr * yr, 1.0);
-        yr = fma_rn(SFB_BMC(kC_Half) * yr, e, yr);
-    }
-    const double s0 = x * yr;
-    const double R = fma_rn(fma_rn(-s0, s0, x), SFB_BMC(kC_Half) * yr, s0);
-    // theta = fl((2 pi NORM) z2) exactly as the reference rounds it
-    const double c = SFB_BMC(kC_TwoPiNorm);
-    const double theta = fma_rn(c, (double)z2m1, c);
+    const double y2 = fma_rn((double)k, SFB_BMC(kC_Neg2Ln2), lc.y);
+    const double x = fma_rn(r2, p, fma_rn(r, SFB_BMC(kC_Neg2), y2));
+    // R = sqrt(x) = x y0 (1 - e)^-1/2 with e = 1 - x y0^2, |e| <= 2^-19 for the
+    // rsqrt.approx seed y0: x y0 (1 + e/2 + 3e^2/8), truncation 5e^3/16 < 2^-58
+    const double y0 = seed(x);
+    const double e = fma_rn(-x, y0 * y0, 1.0);
+    const double s0 = x * y0;
+    const double R = fma_rn(s0 * e, fma_rn(e, SFB_BMC(kC_3o8), SFB_BMC(kC_Half)), s0);
+    // theta = fl((2 pi NORM) z2) exactly as the reference rounds it:
+    // fma(2^52 + z2, c, -2^52 c) is c z2 rounded once (no XU conversion)
+    const double theta = fma_rn(as_f64(0x4330000000000000ull | (z2m1 + 1u)),
+                                SFB_BMC(kC_TwoPiNorm), SFB_BMC(kC_TwoPiNormBias));
     const uint32_t kk = (z2m1 + 1u + (1u << 20)) >> 21;
     const BmPair cs = trigp[kk];
     const double B = theta - angle[kk];  // exact
@@ -273,7 +287,7 @@ SFB_EXP_HD void box_muller_pair_f32_core(uint32_t z1m1, uint32_t z2m1, const BmP
     b = (float)(R * sin_t);
 }
 
-template <int NEWTON, typename SEED = RsqrtSeedHw>
+template <typename SEED = RsqrtSeedHw>
 SFB_EXP_HD void box_muller_pair_f32(uint32_t z1m1, uint32_t z2m1, const BmPair *logp,
                                     const BmPair *trigp, const double *angle,
                                     const uint64_t *logw, const uint64_t *trigw, float &a,
@@ -284,7 +298,7 @@ SFB_EXP_HD void box_muller_pair_f32(uint32_t z1m1, uint32_t z2m1, const BmPair *
         b = p.b;
         return;
     }
-    box_muller_pair_f32_core<NEWTON>(z1m1, z2m1, logp, trigp, angle, a, b, seed);
+    box_muller_pair_f32_core<SEED>(z1m1, z2m1, logp, trigp, angle, a, b, seed);
 }
 
 }  // namespace sfb

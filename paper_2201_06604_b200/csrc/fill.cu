@@ -334,7 +334,6 @@ __global__ void __launch_bounds__(256, MINB) fill_uniform_quad(StateIO io,
 // ops per pair, <= 2^-44 relative) or the float64 transform rounded once
 // (FAST == false, SFB_NORMAL_VARIANT bit 2).
 
-constexpr int kBmF32Newton = 2;  // rsqrt refinements (the seed is only ~2^-20 accurate)
 
 __device__ __forceinline__ void put4(float *p, float a, float b, float c, float d) {
     __stcs((float4 *)p, make_float4(a, b, c, d));
@@ -398,8 +397,7 @@ __device__ __forceinline__ void bm(uint32_t z1, uint32_t z2, const BmView &v, do
 template <bool FAST>
 __device__ __forceinline__ void bm(uint32_t z1, uint32_t z2, const BmView &v, float &a, float &b) {
     if (FAST) {
-        box_muller_pair_f32<kBmF32Newton>(z1, z2, v.logp, v.trigp, v.angle, v.logw, v.trigw, a,
-                                          b);
+        box_muller_pair_f32(z1, z2, v.logp, v.trigp, v.angle, v.logw, v.trigw, a, b);
     } else {
         double da, db;
         box_muller_pair(z1, z2, v.logw, v.trigw, da, db);
@@ -428,7 +426,7 @@ __device__ __forceinline__ void bmN(const uint32_t *z1, const uint32_t *z2, cons
     bool rare = false;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        box_muller_pair_f32_core<kBmF32Newton>(z1[k], z2[k], v.logp, v.trigp, v.angle, a[k], b[k]);
+        box_muller_pair_f32_core(z1[k], z2[k], v.logp, v.trigp, v.angle, a[k], b[k]);
         rare |= bm_f32_needs_exact(z2[k]);
     }
     if (rare) {

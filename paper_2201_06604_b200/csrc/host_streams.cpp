@@ -696,8 +696,10 @@ int sfb_host_box_muller(const int64_t *z1, const int64_t *z2, int64_t n, double 
     return SFB_OK;
 }
 
+// newton: unused (kept for ABI stability; the float32 form has one sqrt path)
 int sfb_host_box_muller_f32(const int64_t *z1, const int64_t *z2, int64_t n, int newton,
                             double seed_rel_err, float *a, float *b) {
+    (void)newton;
     static const uint64_t kLogTab[3 * SFB_BM_LOG_N] = SFB_BM_LOG_TABLE_INIT;
     static const uint64_t kTrigTab[3 * (SFB_BM_TRIG_N + 1)] = SFB_BM_TRIG_TABLE_INIT;
     static std::vector<BmPair> logp(kBmFastLogPairs), trigp(kBmFastTrigPairs);
@@ -710,13 +712,8 @@ int sfb_host_box_muller_f32(const int64_t *z1, const int64_t *z2, int64_t n, int
     for (int64_t k = 0; k < n; ++k) {
         if (z1[k] < 1 || z1[k] > (int64_t)kM1 || z2[k] < 1 || z2[k] > (int64_t)kM1)
             return fail(SFB_E_INVALID_ARGUMENT, "draws must lie in [1, m1]");
-        const uint32_t u1 = (uint32_t)(z1[k] - 1), u2 = (uint32_t)(z2[k] - 1);
-        if (newton >= 2)
-            box_muller_pair_f32<2>(u1, u2, logp.data(), trigp.data(), angle.data(), kLogTab,
-                                   kTrigTab, a[k], b[k], seed);
-        else
-            box_muller_pair_f32<1>(u1, u2, logp.data(), trigp.data(), angle.data(), kLogTab,
-                                   kTrigTab, a[k], b[k], seed);
+        box_muller_pair_f32(uint32_t(z1[k] - 1), uint32_t(z2[k] - 1), logp.data(), trigp.data(),
+                            angle.data(), kLogTab, kTrigTab, a[k], b[k], seed);
     }
     return SFB_OK;
 }
