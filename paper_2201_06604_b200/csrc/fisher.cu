@@ -87,7 +87,7 @@ using LfShared = LfPlain;
 
 // One unit = (item, replicate chunk): its replicates on the item's stream
 // from the chunk's start state; returns the unit's hits.
-template <int WALK, int NR, int NC, typename LF, typename JUMPS>
+template <int WALK, int NR, int NC, bool DSMEM, typename LF, typename JUMPS>
 __device__ __forceinline__ unsigned long long run_unit(const FisherArgs &a, const JUMPS &jumps,
                                                        int64_t u, const int32_t *rowm,
                                                        const int32_t *colm, const LF &lf,
@@ -105,10 +105,11 @@ __device__ __forceinline__ unsigned long long run_unit(const FisherArgs &a, cons
     for (int64_t rep = rep0; rep < rep1; ++rep) {
         double stat;
         if constexpr (NR > 0)  // compile-time shape: column work in registers
-            stat = sample_table_fixed<NR, NC, WALK>(rowm, colm, a.ntot, lf, exptab, s, memo);
+            stat = sample_table_fixed<NR, NC, WALK, DSMEM>(rowm, colm, a.ntot, lf, exptab, s,
+                                                           memo);
         else
-            stat = sample_table<WALK>(rowm, colm, a.nr, a.nc, a.ntot, lf, exptab, s, jw, js,
-                                      nullptr, memo);
+            stat = sample_table<WALK, DSMEM>(rowm, colm, a.nr, a.nc, a.ntot, lf, exptab, s, jw,
+                                             js, nullptr, memo);
         if (stat <= a.threshold) ++uhits;  // _kernels.py:275-276
         if (a.stats) a.stats[local * a.reps + rep] = stat;
     }
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         __syncthreads();
         const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t u = gtid; u < a.nunits; u += gstride)
-            hits += run_unit<WALK, 0, 0>(a, jumps, u, a.rowm, a.colm, LfGlobal{a.lf}, exptab,
+            hits += run_unit<WALK, 0, 0, false>(a, jumps, u, a.rowm, a.colm, LfGlobal{a.lf}, exptab,
                                    a.jwork_global + gtid, (int)a.jstride, a.memo);
     } else {
         const size_t off_row = 2048;
@@ -185,10 +186,10 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
         if (gtid < a.nunits) {  // one unit per thread
             int *jw = (int *)(smem + off_jw) + threadIdx.x;
             if (LF_SMEM)
-                hits = run_unit<WALK, NR, NC>(a, jumps, gtid, srow, scol, LfShared{lfs}, exptab, jw,
+                hits = run_unit<WALK, NR, NC, (NR == 0)>(a, jumps, gtid, srow, scol, LfShared{lfs}, exptab, jw,
                                       (int)blockDim.x, memo);
             else
-                hits = run_unit<WALK, NR, NC>(a, jumps, gtid, srow, scol, LfGlobal{a.lf}, exptab, jw,
+                hits = run_unit<WALK, NR, NC, (NR == 0)>(a, jumps, gtid, srow, scol, LfGlobal{a.lf}, exptab, jw,
                                       (int)blockDim.x, memo);
         }
     }

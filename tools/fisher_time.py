@@ -33,7 +33,8 @@ def case(name, table, n, g, reps):
     ts = []
     for i in range(reps + 3):
         cur.copy_(cur0)
-        if not os.environ.get("NOFLUSH"): scratch.zero_()
+        if os.environ.get("SLEEP"): torch.cuda._sleep(int(os.environ["SLEEP"]))  # warm L2, host launch hidden
+        elif not os.environ.get("NOFLUSH"): scratch.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(); launch_fisher(plan, cur, st.count, cnt); e.record(); e.synchronize()
         if i >= 3: ts.append(s.elapsed_time(e))
@@ -43,6 +44,9 @@ out = {}
 CASES = os.environ.get("CASES", "T4,T10,month,week").split(",")
 for name, table, n, g, reps in [c for c in [("T4", T4, 10**6, (256, 64), 60),
                                 ("T4x10", T4, 10**7, (256, 64), 20),
+                                ("T4n16k", T4, 16384, (256, 64), 60),
+                                ("T4n64k", T4, 65536, (256, 64), 60),
+                                ("T4n256k", T4, 262144, (256, 64), 60),
                                 ("T4x4", T4, 4 * 10**6, (256, 64), 20),
                                 ("T10", G["T10"], (1 << 21) * 8, (2048, 1024), 8),
                                 ("month", A["month"], 10**6, (256, 64), 10),

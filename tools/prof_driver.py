@@ -37,7 +37,7 @@ def uniform(reps=3, kind="uniform"):
     torch.cuda.synchronize()
 
 
-def normal(reps=3, rows=31250 // 8):
+def normal(reps=3, rows=31250 // 4):
     st = sf.create_streams(sf.set_base_creator(), 1 << 18)[0]
     cur = st.device_current()
     out = torch.empty((rows, 32000), dtype=torch.float32, device="cuda")
