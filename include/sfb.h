@@ -135,6 +135,22 @@ int sfb_matern_cov(const double *params, int nb, const double *d_coords, int64_t
 int64_t sfb_matern_scratch_bytes(int nb, int nx, int ny);
 /* CPU test hook: the same K_nu on the host */
 double sfb_host_bessel_k(double nu, double x);
+/* grf.py:190-208 chol_batch: per block LDL^T of `batch` SPD blocks of n x n
+ * (d_a (batch*n, n), row-major, not modified): d_lmat receives the unit-lower
+ * L = C / diag(C) (0 above the diagonal), d_diag (batch, n) D = diag(C)^2, C
+ * the Cholesky factor (LAPACK dpotrf, lower).  d_info (batch) int32: 0, or
+ * LAPACK's info -- the order of the first non-positive leading minor -- for a
+ * block that is not positive definite (the caller raises
+ * NotPositiveDefiniteError(batch, pivot)).  Hand-written FP64 tensor-core
+ * (DMMA) blocked factorisation; d_lmat may alias d_a. */
+int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, double *d_diag,
+                   int32_t *d_info, void *stream);
+/* grf.py:211-240 multiply_lower_diag_batch: d_out (batch*n, r) block b =
+ * L_b diag(s(D_b)) Z_b, s = sqrt (transform 0) or identity (1); d_z (n, r)
+ * shared by every block (z_shared = 1) or (batch*n, r). */
+int sfb_lower_diag_multiply(const double *d_lmat, const double *d_diag, int64_t n, int64_t batch,
+                            const double *d_z, int z_shared, int64_t r, int transform,
+                            double *d_out, void *stream);
 
 /* multi-GPU e2e helper (no reference counterpart: the reference has one host):
  * copy the cells of grid columns [j_lo, j_hi) -- columns c = j + g1 q of a

@@ -63,6 +63,8 @@ _SIGS = {
     "sfb_matern_cov": ([_f64p, _int, _vp, _i64, _int, _int, ctypes.c_double, _vp, _vp, _vp], _int),
     "sfb_matern_scratch_bytes": ([_int, _int, _int], _i64),
     "sfb_host_bessel_k": ([ctypes.c_double, ctypes.c_double], ctypes.c_double),
+    "sfb_chol_batch": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp], _int),
+    "sfb_lower_diag_multiply": ([_vp, _vp, _i64, _i64, _vp, _int, _i64, _int, _vp, _vp], _int),
     "sfb_download_shard": ([_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp], _int),
     "sfb_probe_write": ([_vp, _i64, _int, _vp], _int),
     "sfb_host_step_u32": ([_i64p, _i64, _i64, _i64p], _int),

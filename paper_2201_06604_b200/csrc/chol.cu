@@ -1,0 +1,649 @@
+// chol.cu -- batched FP64 Cholesky LDL^T and the L D^1/2 Z contraction of the
+// Gaussian-random-field pipeline (reference
+// grf.py:190-240 chol_batch / multiply_lower_diag_batch).
+//
+// The reference factors each covariance block with LAPACK dpotrf (C C^T,
+// lower), then L = C / diag(C) (unit lower), D = diag(C)^2, and multiplies
+// L diag(sqrt D) Z with numpy.  Here, per batch of B blocks of n x n (row-major,
+// block b at a + b n^2), all on the device with hand-written kernels:
+//
+//   * blocked right-looking Cholesky on 64 x 64 tiles, one launch per stage and
+//     panel k, every launch covering all B blocks (grid.y = batch):
+//       chol_diag    -- factor tile (k, k) in shared memory (unblocked, rank-1
+//                       updates) and invert it (row-wise substitution);
+//       chol_trsm    -- panel tiles (I, k), I > k:  A_Ik <- A_Ik L_kk^-T as a
+//                       64 x 64 x 64 product with the inverse (the TRSM-by-
+//                       inverse of GPU LAPACKs);
+//       chol_update  -- trailing tiles (I, J), k < J <= I:
+//                       A_IJ <- A_IJ - A_Ik A_Jk^T;
+//     the two products run on the FP64 tensor cores (mma.sync m8n8k4 f64,
+//     DMMA), 64 x 64 output tile per CTA, 4 warps of 32 x 32, operands staged
+//     in shared memory with a 68-double row pitch (conflict-free fragment
+//     loads);
+//   * chol_finish    -- L = C / diag(C) below the diagonal, 1 on it, 0 above;
+//                       D = diag(C)^2 (grf.py:203-207);
+//   * lower_diag_mul -- out = L diag(s) Z, s = sqrt(D) or D: one warp per
+//                       output row, the row of L read once (HBM-bound).
+// A non-positive (or NaN) pivot stops that block: info[b] = LAPACK's info (the
+// 1-based order of the first non-positive leading minor), and the later
+// stages skip the block.  Results match LAPACK/numpy within rounding (the
+// summation order differs), which is how the reference's own tests compare.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+
+#include "sfb_internal.h"
+
+namespace sfb {
+
+constexpr int kT = 64;        // tile
+constexpr int kPitch = 68;    // shared-memory row pitch in doubles (64 + 4)
+constexpr int kGemmThreads = 128;
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// rows [r0, r0 + rows) x 64 columns at column c0 of block `blk` (pitch n) into
+// shared s[64][kPitch]; rows past `rows` are zero
+__device__ __forceinline__ void load_tile(double *s, const double *blk, int64_t n, int64_t r0,
+                                          int rows, int64_t c0, int cols) {
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+        const int r = e >> 6, c = e & 63;
+        s[r * kPitch + c] = (r < rows && c < cols) ? blk[(r0 + r) * n + c0 + c] : 0.0;
+    }
+}
+
+// acc (this warp's 32 x 32 quarter of a 64 x 64 tile, 4 x 4 DMMA tiles of
+// 8 x 8, two doubles per lane each) = sa[0:64, 0:64] * sb[0:64, 0:64]^T
+__device__ __forceinline__ void tile_product(const double *sa, const double *sb,
+                                             double (&acc)[4][4][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+    const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < kT; k0 += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sa[(wr + 8 * i + fr) * kPitch + k0 + fk];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = sb[(wc + 8 * j + fr) * kPitch + k0 + fk];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+}
+
+// Factor tile (k, k) of every block and store the inverse of its lower factor.
+// The tile's factorisation is on the critical path of every panel step, so
+// each of its 64 steps is spread over 1024 threads: thread t owns elements t,
+// t + 1024 and t + 2048 of the 2080-element lower triangle, and a step is two barriers
+// apart (the owner of row j takes the square root and its reciprocal, the
+// column is scaled, the trailing triangle gets its rank-1 update).  The inverse
+// X = L^-1 is computed the same way, right-looking on L X = I.  Loops stay
+// rolled: unrolled register-resident forms are tens of thousands of
+// straight-line instructions, and instruction fetch ("no_instructions"
+// stalls) made them slower than this (measured 113-200 us vs ~10 us).
+constexpr int kTri = kT * (kT + 1) / 2;  // 2080
+constexpr int kDiagSmem = 2 * kT * (kT + 1) * (int)sizeof(double);
+
+template <int kDiagThreads>
+__global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, int k, int *info,
+                                                          double *linv) {
+    extern __shared__ double dsm[];
+    double(*s)[kT + 1] = (double(*)[kT + 1])dsm;                    // tile -> L
+    double(*x)[kT + 1] = (double(*)[kT + 1])(dsm + kT * (kT + 1));  // X = L^-1
+    const int b = blockIdx.y;
+    if (info[b]) return;
+    double *blk = a + (int64_t)b * n * n;
+    const int64_t o = (int64_t)k * kT;
+    const int m = (int)(n - o < kT ? n - o : kT);
+    const int t = threadIdx.x;
+    // rows/columns past the block factor as the identity; X starts as I
+    for (int e = t; e < kT * kT; e += kDiagThreads) {
+        const int rr = e >> 6, c = e & 63;
+        s[rr][c] = (rr < m && c < m) ? blk[(o + rr) * n + o + c] : (rr == c ? 1.0 : 0.0);
+        x[rr][c] = rr == c ? 1.0 : 0.0;
+    }
+    // this thread's triangle elements (r, l), l <= r (r = -1: none)
+    constexpr int kPer = (kTri + kDiagThreads - 1) / kDiagThreads;  // 3
+    int er[kPer], el[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int e = t + q * kDiagThreads;
+        if (e < kTri) {
+            int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+            while (r * (r + 1) / 2 > e) --r;
+            while ((r + 1) * (r + 2) / 2 <= e) ++r;
+            er[q] = r;
+            el[q] = e - r * (r + 1) / 2;
+        } else {
+            er[q] = -1;
+            el[q] = 0;
+        }
+    }
+    __shared__ double rinv[kT];  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
+    __shared__ int bad;
+    if (t == 0) bad = 0;
+    __syncthreads();
+    for (int j = 0; j < kT; ++j) {
+        if (t == j) {
+            const double d = s[j][j];
+            if (!(d > 0.0)) {
+                bad = j + 1;
+            } else {
+                const double ljj = sqrt(d);
+                s[j][j] = ljj;
+                rinv[j] = 1.0 / ljj;
+            }
+        }
+        __syncthreads();
+        if (bad) break;
+        if (t > j && t < kT) s[t][j] *= rinv[j];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+            if (el[q] > j) s[er[q]][el[q]] -= s[er[q]][j] * s[el[q]][j];
+        __syncthreads();
+    }
+    if (bad) {
+        if (t == 0) info[b] = (int)(o + bad);  // LAPACK info: order of the failing minor
+        return;
+    }
+    // L X = I, right-looking: row j of X scaled by 1 / L[j][j], then subtracted
+    // from the rows below; the columns c <= j of X are the only nonzero ones
+    for (int j = 0; j < kT; ++j) {
+        if (t <= j) x[j][t] *= rinv[j];
+        __syncthreads();
+        for (int e = t; e < (kT - 1 - j) * (j + 1); e += kDiagThreads) {
+            const int r = j + 1 + e / (j + 1), c = e % (j + 1);
+            x[r][c] -= s[r][j] * x[j][c];
+        }
+        __syncthreads();
+    }
+    for (int e = t; e < kT * kT; e += kDiagThreads) {
+        const int rr = e >> 6, c = e & 63;
+        if (rr < m && c <= rr) blk[(o + rr) * n + o + c] = s[rr][c];
+    }
+    double *li = linv + (int64_t)b * kT * kT;
+    for (int e = t; e < kT * kT; e += kDiagThreads) li[e] = x[e >> 6][e & 63];
+}
+
+// Panel: A_Ik <- A_Ik L_kk^-T for the tiles I > k below the diagonal.
+__global__ void __launch_bounds__(kGemmThreads) chol_trsm(double *a, int64_t n, int k,
+                                                          const int *info, const double *linv) {
+    extern __shared__ double sm[];
+    double *sa = sm, *sb = sm + kT * kPitch;
+    const int b = blockIdx.y;
+    if (info[b]) return;
+    double *blk = a + (int64_t)b * n * n;
+    const int64_t I = (int64_t)k + 1 + blockIdx.x;
+    const int64_t r0 = I * kT, c0 = (int64_t)k * kT;
+    const int rows = (int)(n - r0 < kT ? n - r0 : kT);
+    load_tile(sa, blk, n, r0, rows, c0, kT);
+    const double *li = linv + (int64_t)b * kT * kT;
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x)
+        sb[(e >> 6) * kPitch + (e & 63)] = li[e];
+    __syncthreads();
+    double acc[4][4][2];
+    tile_product(sa, sb, acc);  // A_Ik Linv^T: B[q][c] = Linv[c][q]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = wr + 8 * i + (lane >> 2);
+        if (rr >= rows) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cc = wc + 8 * j + 2 * (lane & 3);
+            double *p = blk + (r0 + rr) * n + c0 + cc;
+            p[0] = acc[i][j][0];
+            p[1] = acc[i][j][1];
+        }
+    }
+}
+
+// Update of the tiles (I, J), J in [j_lo, j_hi), I in [J, nt):
+//   A_IJ -= sum_{k in [k_lo, k_hi)} A_Ik A_Jk^T
+// (the panel-local updates inside a super-panel, K = one tile, and the delayed
+// trailing update after it, K = the super-panel).  K is streamed in slices of
+// 32 columns through a two-stage cp.async pipeline (16-byte copies; rows past
+// the block are zero-filled by the copy); VEC == false (odd n, unaligned rows)
+// loads synchronously.
+constexpr int kSlice = 32;
+constexpr int kSPitch = kSlice + 4;  // conflict-free fragment loads
+constexpr int kStages = 2;  // cp.async pipeline depth (3: 110 KB per CTA, slower -- the chain kernels no longer fit beside the bulk update)
+constexpr int kUpdSmem = kStages * 2 * kT * kSPitch * (int)sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, int src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+
+template <bool VEC>
+__device__ __forceinline__ void load_slice(double *sa, const double *blk, int64_t n, int64_t r0,
+                                           int rows, int64_t c0) {
+    if (VEC) {
+        for (int e = threadIdx.x; e < kT * kSlice / 2; e += blockDim.x) {
+            const int rr = e >> 4, cc = (e & 15) * 2;
+            const bool in = rr < rows;
+            cp_async16(sa + rr * kSPitch + cc, blk + (r0 + (in ? rr : 0)) * n + c0 + cc, in ? 16 : 0);
+        }
+    } else {
+        for (int e = threadIdx.x; e < kT * kSlice; e += blockDim.x) {
+            const int rr = e >> 5, cc = e & 31;
+            sa[rr * kSPitch + cc] = rr < rows ? blk[(r0 + rr) * n + c0 + cc] : 0.0;
+        }
+    }
+}
+
+// Persistent: CTAs stride over the linear index of (batch, J, I) tiles, so a
+// launch can be held to a fixed number of CTAs per SM (the bulk update leaves
+// room for the serial chain's kernels next to it).
+template <bool VEC>
+__global__ void __launch_bounds__(kGemmThreads) chol_update(double *a, int64_t n, int nt, int k_lo,
+                                                            int k_hi, int j_lo, int j_hi,
+                                                            int batch, const int *info) {
+    extern __shared__ double sm[];
+    const int64_t R = nt - j_lo, per = R * (j_hi - j_lo);
+    for (int64_t x = blockIdx.x; x < per * batch; x += gridDim.x) {
+        const int b = (int)(x / per);
+        const int64_t y = x - b * per;
+        const int64_t I = j_lo + y % R, J = j_lo + y / R;
+        if (I < J || info[b]) continue;  // uniform per CTA
+        double *blk = a + (int64_t)b * n * n;
+        const int64_t ri = I * kT, rj = J * kT;
+        const int rows = (int)(n - ri < kT ? n - ri : kT);
+        const int cols = (int)(n - rj < kT ? n - rj : kT);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+        const int fr = lane >> 2, fk = lane & 3;
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        const int nsl = (k_hi - k_lo) * (kT / kSlice);
+        const int64_t kc0 = (int64_t)k_lo * kT;
+        auto stage = [&](int st) { return sm + st * 2 * kT * kSPitch; };
+        // prologue: slices 0 .. kStages-2 in flight; one commit group per slice
+        // (empty groups past the end keep the wait_group arithmetic uniform)
+#pragma unroll
+        for (int q = 0; q < kStages - 1; ++q) {
+            if (q < nsl) {
+                load_slice<VEC>(stage(q), blk, n, ri, rows, kc0 + (int64_t)q * kSlice);
+                load_slice<VEC>(stage(q) + kT * kSPitch, blk, n, rj, cols, kc0 + (int64_t)q * kSlice);
+            }
+            if (VEC) asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int nx = sl + kStages - 1;  // refill the stage consumed at sl - 1
+            if (nx < nsl) {
+                double *sg = stage(nx % kStages);
+                load_slice<VEC>(sg, blk, n, ri, rows, kc0 + (int64_t)nx * kSlice);
+                load_slice<VEC>(sg + kT * kSPitch, blk, n, rj, cols, kc0 + (int64_t)nx * kSlice);
+            }
+            if (VEC) {
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
+            }
+            __syncthreads();
+            const double *sa = stage(sl % kStages), *sb = sa + kT * kSPitch;
+#pragma unroll
+            for (int k0 = 0; k0 < kSlice; k0 += 4) {
+                double fa[4], fb[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) fa[i] = sa[(wr + 8 * i + fr) * kSPitch + k0 + fk];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) fb[j] = sb[(wc + 8 * j + fr) * kSPitch + k0 + fk];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+            }
+            __syncthreads();  // the stage is refilled at the next iteration
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int rr = wr + 8 * i + fr;
+            if (rr >= rows) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cc = wc + 8 * j + 2 * fk;
+                double *p = blk + (ri + rr) * n + rj + cc;
+                if (cc < cols) p[0] -= acc[i][j][0];
+                if (cc + 1 < cols) p[1] -= acc[i][j][1];
+            }
+        }
+    }
+}
+
+// L = C / diag(C) below the diagonal, 1 on it, 0 above; D = diag(C)^2
+// (grf.py:203-207), in place on the factored blocks.
+__global__ void chol_finish(double *c, double *diag, int64_t n, const int *info) {
+    const int b = blockIdx.y;
+    if (info[b]) return;
+    double *blk = c + (int64_t)b * n * n;
+    const int64_t total = n * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        if (j < i) {
+            blk[e] = blk[e] / blk[j * n + j];  // reads the untouched diagonal C_jj
+        } else if (j > i) {
+            blk[e] = 0.0;
+        }
+    }
+}
+
+__global__ void chol_diag_out(double *c, double *diag, int64_t n, const int *info) {
+    const int b = blockIdx.y;
+    if (info[b]) return;
+    double *blk = c + (int64_t)b * n * n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = blk[i * n + i];
+        diag[(int64_t)b * n + i] = d * d;
+        blk[i * n + i] = 1.0;
+    }
+}
+
+// w[b][j][c] = s(D[b][j]) Z[bz][j][c], s = sqrt (transform 0) or identity
+__global__ void scale_rows(const double *diag, const double *z, int z_shared, int64_t n,
+                           int64_t r, int transform, double *w) {
+    const int b = blockIdx.y;
+    const double *zb = z + (z_shared ? 0 : (int64_t)b * n * r);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * r;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const double d = diag[(int64_t)b * n + e / r];
+        w[(int64_t)b * n * r + e] = (transform == 0 ? sqrt(d) : d) * zb[e];
+    }
+}
+
+// out[b][i][c] = sum_{j <= i} L[b][i][j] w[b][j][c]: one warp per row i,
+// RC columns of w per pass
+template <int RC>
+__global__ void __launch_bounds__(256) lower_mul(const double *lmat, const double *w, int64_t n,
+                                                 int64_t r, int64_t c0, double *out) {
+    const int b = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const double *li = lmat + (int64_t)b * n * n + i * n;
+    const double *wb = w + (int64_t)b * n * r + c0;
+    const int rc = (int)(r - c0 < RC ? r - c0 : RC);
+    double acc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+    // four row elements per lane in flight (independent loads), then the FMAs
+    int64_t j = lane;
+    for (; j + 96 <= i; j += 128) {
+        double l[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) l[u] = __ldg(li + j + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double *wj = wb + (j + 32 * u) * r;
+#pragma unroll
+            for (int c = 0; c < RC; ++c)
+                if (c < rc) acc[c] += l[u] * __ldg(wj + c);
+        }
+    }
+    for (; j <= i; j += 32) {
+        const double l = __ldg(li + j);
+        const double *wj = wb + j * r;
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+            if (c < rc) acc[c] += l * __ldg(wj + c);
+    }
+#pragma unroll
+    for (int c = 0; c < RC; ++c)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if (lane == 0) {
+        double *ob = out + (int64_t)b * n * r + i * r + c0;
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+            if (c < rc) ob[c] = acc[c];
+    }
+}
+
+// Grow-only per-device scratch (a cudaMallocAsync / cudaFreeAsync pair per
+// call measured 0.4 -> 3.3 ms of variance: the pool hands memory back and
+// re-maps it).  A reuse on another stream waits for the last use's event.
+struct Scratch {
+    std::mutex mu;
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t last = nullptr;
+    bool used = false;
+};
+
+static Scratch &scratch(int dev, int which) {
+    static Scratch sc[64][2];
+    return sc[dev & 63][which & 1];
+}
+
+// call with sc.mu held; the returned buffer is valid for work enqueued on st
+// until release()
+static cudaError_t acquire(Scratch &sc, size_t bytes, cudaStream_t st, void **out) {
+    cudaError_t e = cudaSuccess;
+    if (!sc.last) e = cudaEventCreateWithFlags(&sc.last, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    if (bytes > sc.cap) {
+        if (sc.used) e = cudaEventSynchronize(sc.last);  // the old buffer's last reader
+        if (e == cudaSuccess && sc.p) e = cudaFree(sc.p);
+        sc.p = nullptr;
+        sc.cap = 0;
+        if (e == cudaSuccess) e = cudaMalloc(&sc.p, bytes);
+        if (e != cudaSuccess) return e;
+        sc.cap = bytes;
+        sc.used = false;
+    }
+    if (sc.used) e = cudaStreamWaitEvent(st, sc.last, 0);
+    *out = sc.p;
+    return e;
+}
+
+static void release(Scratch &sc, cudaStream_t st) {
+    cudaEventRecord(sc.last, st);
+    sc.used = true;
+}
+
+struct LookAhead {
+    std::mutex mu;
+    cudaStream_t sb = nullptr, sh = nullptr;  // bulk update (low priority), chain (high)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s = nullptr;
+};
+
+static LookAhead &look_ahead(int dev) {
+    static LookAhead la[64];
+    return la[dev & 63];
+}
+
+}  // namespace sfb
+
+using namespace sfb;
+
+extern "C" {
+
+int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, double *d_diag,
+                   int32_t *d_info, void *stream) {
+    if (n < 1 || batch < 1) return fail(SFB_E_INVALID_ARGUMENT, "need n >= 1 and batch >= 1");
+    if (batch > 65535) return fail(SFB_E_INVALID_ARGUMENT, "at most 65535 blocks per call");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = (size_t)batch * n * n * sizeof(double);
+    cudaError_t e = cudaMemsetAsync(d_info, 0, sizeof(int32_t) * batch, st);
+    if (e == cudaSuccess && d_lmat != d_a)
+        e = cudaMemcpyAsync(d_lmat, d_a, bytes, cudaMemcpyDeviceToDevice, st);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Scratch &sc = scratch(dev, 0);
+    std::lock_guard<std::mutex> slock(sc.mu);
+    double *linv = nullptr;
+    if (e == cudaSuccess) e = acquire(sc, sizeof(double) * kT * kT * batch, st, (void **)&linv);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch setup: %s", cudaGetErrorString(e));
+    // dynamic shared-memory limits, raised once per device
+    static std::atomic<uint64_t> done{0};
+    const int smem = 2 * kT * kPitch * (int)sizeof(double);
+    if (!(done.load() & (1ull << (dev & 63)))) {
+        e = cudaFuncSetAttribute(chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kUpdSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_update<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_diag<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kDiagSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_diag<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kDiagSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_diag<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kDiagSmem);
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch attributes: %s", cudaGetErrorString(e));
+        done.fetch_or(1ull << (dev & 63));
+    }
+    int *info = (int *)d_info;
+    const int nt = (int)((n + kT - 1) / kT);
+    // right-looking over super-panels of W tiles: inside a super-panel each
+    // 64-column step factors its diagonal tile, solves its whole column below
+    // and updates only the super-panel's later columns; the rest of the
+    // trailing matrix gets one delayed update with K = the super-panel
+    const int W = std::max(1, tune_knob("SFB_CHOL_PANEL", 8));
+    const bool vec = (n % 2) == 0;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int bulk_per_sm = std::max(1, tune_knob("SFB_CHOL_BULK_CTAS", 2));
+    // cap: CTAs per launch (the bulk update: bulk_per_sm per SM)
+    auto update = [&](cudaStream_t us, int k_lo, int k_hi, int j_lo, int j_hi, int cap) {
+        const int64_t tiles = (int64_t)(nt - j_lo) * (j_hi - j_lo) * batch;
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, cap);
+        if (vec)
+            chol_update<true><<<grid, kGemmThreads, kUpdSmem, us>>>(d_lmat, n, nt, k_lo, k_hi,
+                                                                   j_lo, j_hi, (int)batch, info);
+        else
+            chol_update<false><<<grid, kGemmThreads, kUpdSmem, us>>>(d_lmat, n, nt, k_lo, k_hi,
+                                                                    j_lo, j_hi, (int)batch, info);
+    };
+    const int cap_all = 1 << 30, cap_bulk = nsm * bulk_per_sm;
+    const int diag_threads = tune_knob("SFB_CHOL_DIAG_THREADS", 512);
+    // Look-ahead: after super-panel i is factored, its update of the next
+    // super-panel's columns (a_i) runs on the caller's stream, the bulk update
+    // of everything beyond (b_i) on a second stream, where it overlaps the
+    // factorisation of super-panel i + 1 (the serial diag/trsm chain).  a_i
+    // touches the tiles b_{i-1} updated, so it waits for b_{i-1}; b_i waits for
+    // super-panel i's factors.  Per device: the second stream and two events,
+    // used under a lock (the enqueue sequence of one call is atomic).
+    // The serial chain runs on a high-priority stream (the block scheduler
+    // then dispatches its small grids ahead of the bulk update's pending CTAs).
+    LookAhead &la = look_ahead(dev);
+    std::lock_guard<std::mutex> lock(la.mu);
+    if (!la.sb) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&la.sb, cudaStreamNonBlocking, lo);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&la.sh, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_a, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_b, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_s, cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch streams: %s", cudaGetErrorString(e));
+    }
+    const cudaStream_t caller = st;
+    cudaEventRecord(la.ev_s, caller);  // the copy into d_lmat, the info reset, linv
+    cudaStreamWaitEvent(la.sh, la.ev_s, 0);
+    st = la.sh;
+    bool pending_b = false;
+    for (int p0 = 0; p0 < nt && e == cudaSuccess; p0 += W) {
+        const int p1 = std::min(p0 + W, nt), p2 = std::min(p1 + W, nt);
+        for (int k = p0; k < p1; ++k) {
+            if (diag_threads == 256)
+                chol_diag<256><<<dim3(1, (unsigned)batch), 256, kDiagSmem, st>>>(d_lmat, n, k, info,
+                                                                                 linv);
+            else if (diag_threads == 512)
+                chol_diag<512><<<dim3(1, (unsigned)batch), 512, kDiagSmem, st>>>(d_lmat, n, k, info,
+                                                                                 linv);
+            else
+                chol_diag<1024><<<dim3(1, (unsigned)batch), 1024, kDiagSmem, st>>>(d_lmat, n, k,
+                                                                                   info, linv);
+            if (k + 1 < nt)
+                chol_trsm<<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads, smem, st>>>(
+                    d_lmat, n, k, info, linv);
+            if (k + 1 < p1) update(st, k, k + 1, k + 1, p1, cap_all);
+        }
+        if (p1 < nt) {
+            cudaEventRecord(la.ev_a, st);  // super-panel p0 factored
+            if (pending_b) cudaStreamWaitEvent(st, la.ev_b, 0);  // b of the previous super-panel
+            update(st, p0, p1, p1, p2, cap_all);  // a: the next super-panel's columns
+            if (p2 < nt) {
+                cudaStreamWaitEvent(la.sb, la.ev_a, 0);
+                update(la.sb, p0, p1, p2, nt, cap_bulk);  // b: the rest
+                cudaEventRecord(la.ev_b, la.sb);
+                pending_b = true;
+            } else {
+                pending_b = false;
+            }
+        }
+        e = cudaGetLastError();
+    }
+    if (pending_b) cudaStreamWaitEvent(st, la.ev_b, 0);
+    cudaEventRecord(la.ev_s, st);
+    cudaStreamWaitEvent(caller, la.ev_s, 0);
+    st = caller;
+    if (e == cudaSuccess) {
+        const unsigned g = (unsigned)std::min<int64_t>(1184, (n * n + 255) / 256);
+        chol_finish<<<dim3(g, (unsigned)batch), 256, 0, st>>>(d_lmat, d_diag, n, info);
+        chol_diag_out<<<dim3((unsigned)((n + 255) / 256), (unsigned)batch), 256, 0, st>>>(
+            d_lmat, d_diag, n, info);
+        e = cudaGetLastError();
+    }
+    release(sc, st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+int sfb_lower_diag_multiply(const double *d_lmat, const double *d_diag, int64_t n, int64_t batch,
+                            const double *d_z, int z_shared, int64_t r, int transform,
+                            double *d_out, void *stream) {
+    if (n < 1 || batch < 1 || r < 1) return fail(SFB_E_INVALID_ARGUMENT, "empty operands");
+    if (transform != 0 && transform != 1)
+        return fail(SFB_E_INVALID_ARGUMENT, "transform must be 'sqrt' or 'identity'");
+    if (batch > 65535) return fail(SFB_E_INVALID_ARGUMENT, "at most 65535 blocks per call");
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Scratch &sc = scratch(dev, 1);
+    std::lock_guard<std::mutex> slock(sc.mu);
+    double *w = nullptr;
+    cudaError_t e = acquire(sc, sizeof(double) * batch * n * r, st, (void **)&w);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "lower_diag_multiply: %s", cudaGetErrorString(e));
+    const unsigned g = (unsigned)std::min<int64_t>(1184, (n * r + 255) / 256);
+    scale_rows<<<dim3(g, (unsigned)batch), 256, 0, st>>>(d_diag, d_z, z_shared, n, r, transform, w);
+    const unsigned rows_per_cta = 8;
+    for (int64_t c0 = 0; c0 < r; c0 += 8) {
+        const dim3 grid((unsigned)((n + rows_per_cta - 1) / rows_per_cta), (unsigned)batch);
+        if (r - c0 <= 2)
+            lower_mul<2><<<grid, 256, 0, st>>>(d_lmat, w, n, r, c0, d_out);
+        else
+            lower_mul<8><<<grid, 256, 0, st>>>(d_lmat, w, n, r, c0, d_out);
+    }
+    e = cudaGetLastError();
+    release(sc, st);
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "lower_diag_multiply: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
+
+}  // extern "C"

@@ -178,6 +178,61 @@ def test_not_positive_definite_names_batch_and_pivot():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n,nb", [(1, 1), (63, 2), (64, 1), (65, 3), (129, 2), (333, 2), (600, 1)])
+def test_chol_batch_tiles_odd_and_ragged_sizes(n, nb):
+    """csrc/chol.cu on sizes around its 64-tile grid (ragged last tile; odd n:
+    the synchronous loader) against the oracle (scipy LAPACK), grf.py:190-208."""
+    rng = np.random.default_rng(n)
+    blocks = []
+    for _ in range(nb):
+        a = rng.standard_normal((n, n))
+        blocks.append(a @ a.T + n * np.eye(n))  # SPD, well conditioned
+    data = np.vstack(blocks)
+    lmat, diag = sf.chol_batch(BatchedMatrix(data, nb))
+    rl, rd = og.chol_batch(data, nb)
+    assert np.allclose(lmat.data, rl, rtol=1e-10, atol=1e-12)
+    assert np.allclose(diag.data, rd, rtol=1e-10, atol=1e-12)
+    for b in range(nb):
+        lb = lmat.block(b)
+        assert np.array_equal(np.triu(lb, 1), np.zeros((n, n)))
+        assert np.array_equal(np.diag(lb), np.ones(n))
+
+
+@pytest.mark.gpu
+def test_not_positive_definite_pivot_in_a_later_tile():
+    """The first failing minor lies past the first 64-tile (LAPACK info = its
+    order); the other blocks of the batch are unaffected by the failure."""
+    n = 150
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((n, n))
+    good = a @ a.T + n * np.eye(n)
+    bad = good.copy()
+    bad[100:, 100:] -= 1e6 * np.eye(n - 100)  # minor of order 101 is negative
+    with pytest.raises(NotPositiveDefiniteError) as exc:
+        sf.chol_batch(BatchedMatrix(np.vstack([good, bad, good]), 3))
+    assert exc.value.batch == 1 and exc.value.pivot == 101
+
+
+@pytest.mark.gpu
+def test_multiply_lower_diag_batch_many_realisations_against_numpy():
+    """R = 11 (the 8-column passes plus a remainder), Z shared and per block."""
+    rng = np.random.default_rng(5)
+    n, nb, r = 97, 3, 11
+    lm = np.tril(rng.standard_normal((nb, n, n)), -1) + np.eye(n)
+    d = rng.uniform(0.5, 2.0, (nb, n))
+    for zrows in (n, nb * n):
+        z = rng.standard_normal((zrows, r))
+        for tr in ("sqrt", "identity"):
+            out = sf.multiply_lower_diag_batch(BatchedMatrix(lm.reshape(nb * n, n), nb),
+                                               DiagBatch(d), z, transform=tr)
+            for b in range(nb):
+                zb = z if zrows == n else z[b * n:(b + 1) * n]
+                s = np.sqrt(d[b]) if tr == "sqrt" else d[b]
+                ref = lm[b] @ (s[:, None] * zb)
+                assert np.allclose(out.block(b), ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.gpu
 def test_multiply_lower_diag_batch_cases():
     out = sf.multiply_lower_diag_batch(BatchedMatrix(np.eye(3), 1), DiagBatch(np.ones((1, 3))),
                                        np.arange(6.0).reshape(3, 2))
