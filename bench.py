@@ -792,7 +792,7 @@ def main():
                                            config="configs[3]/C4: T10, 1e10 -> 10001317888 "
                                                   "tables on grid (2048,1024), 2^21 streams")
     if args.only is None and rank == 0:
-        run_grf(sf, 1)  # warm-up (cuSOLVER workspaces, kernels)
+        run_grf(sf, 1)  # warm-up (scratch buffers, look-ahead streams, kernels)
         s_grf = run_grf(sf, 3)
         workloads["grf_4x5130"] = dict(value=1.0 / s_grf, unit="GRF batches/s",
                                        ms_per_step=1e3 * s_grf,
