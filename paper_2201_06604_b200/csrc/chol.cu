@@ -235,10 +235,15 @@ template <bool VEC>
 __device__ __forceinline__ void load_slice(double *sa, const double *blk, int64_t n, int64_t r0,
                                            int rows, int64_t c0) {
     if (VEC) {
-        for (int e = threadIdx.x; e < kT * kSlice / 2; e += blockDim.x) {
-            const int rr = e >> 4, cc = (e & 15) * 2;
-            const bool in = rr < rows;
-            cp_async16(sa + rr * kSPitch + cc, blk + (r0 + (in ? rr : 0)) * n + c0 + cc, in ? 16 : 0);
+        // thread t copies columns cc, cc + 1 of rows t/16 + 8q (q < 8): one
+        // base pointer, the row step is a constant
+        const int rr0 = threadIdx.x >> 4, cc = (threadIdx.x & 15) * 2;
+        const double *src = blk + (r0 + rr0) * n + c0 + cc;
+        double *dst = sa + rr0 * kSPitch + cc;
+#pragma unroll
+        for (int q = 0; q < kT * kSlice / 2 / kGemmThreads; ++q) {
+            const bool in = rr0 + 8 * q < rows;
+            cp_async16(dst + 8 * q * kSPitch, in ? src + 8 * q * n : src, in ? 16 : 0);
         }
     } else {
         for (int e = threadIdx.x; e < kT * kSlice; e += blockDim.x) {
@@ -314,18 +319,33 @@ __global__ void __launch_bounds__(kGemmThreads) chol_update(double *a, int64_t n
             }
             __syncthreads();  // the stage is refilled at the next iteration
         }
+        // C -= acc: every load first (32 in flight), then the stores (a
+        // read-modify-write per element serialises on possible aliasing:
+        // measured 86 % of the stall samples)
+        double cv[4][4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int rr = wr + 8 * i + fr;
-            if (rr >= rows) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cc = wc + 8 * j + 2 * fk;
+                const double *p = blk + (ri + rr) * n + rj + cc;
+                cv[i][j][0] = (rr < rows && cc < cols) ? p[0] : 0.0;
+                cv[i][j][1] = (rr < rows && cc + 1 < cols) ? p[1] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int rr = wr + 8 * i + fr;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int cc = wc + 8 * j + 2 * fk;
                 double *p = blk + (ri + rr) * n + rj + cc;
-                if (cc < cols) p[0] -= acc[i][j][0];
-                if (cc + 1 < cols) p[1] -= acc[i][j][1];
+                if (rr < rows && cc < cols) p[0] = cv[i][j][0] - acc[i][j][0];
+                if (rr < rows && cc + 1 < cols) p[1] = cv[i][j][1] - acc[i][j][1];
             }
         }
+        __syncthreads();  // the next tile's prologue refills the stages
     }
 }
 
