@@ -85,55 +85,37 @@ __device__ __forceinline__ void tile_product(const double *sa, const double *sb,
 }
 
 // Factor tile (k, k) of every block and store the inverse of its lower factor.
-// The tile's factorisation is on the critical path of every panel step, so
-// each of its 64 steps is spread over 1024 threads: thread t owns elements t,
-// t + 1024 and t + 2048 of the 2080-element lower triangle, and a step is two barriers
-// apart (the owner of row j takes the square root and its reciprocal, the
-// column is scaled, the trailing triangle gets its rank-1 update).  The inverse
-// X = L^-1 is computed the same way, right-looking on L X = I.  Loops stay
-// rolled: unrolled register-resident forms are tens of thousands of
-// straight-line instructions, and instruction fetch ("no_instructions"
-// stalls) made them slower than this (measured 113-200 us vs ~10 us).
-constexpr int kTri = kT * (kT + 1) / 2;  // 2080
+// The tile's factorisation is on the critical path of every panel step.  512
+// threads: warp w owns rows 4w .. 4w + 3, lane l columns l and l + 32.  Step j
+// is three barriers long: the owner of row j takes the square root and its
+// reciprocal; column j is scaled; then every row r > j updates its trailing
+// part (columns j < l <= r) and, in the same pass, row r of X = L^-1 (L X = I
+// right-looking: columns l <= j, X's row j final) -- warps whose rows all lie
+// above j skip the pass.  Loops stay rolled: unrolled register-resident forms
+// are tens of thousands of straight-line instructions and stalled on
+// instruction fetch (measured 113-200 us per tile).
+constexpr int kDiagThreads = 512;
 constexpr int kDiagSmem = 2 * kT * (kT + 1) * (int)sizeof(double);
 
-template <int kDiagThreads>
 __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, int k, int *info,
                                                           double *linv) {
     extern __shared__ double dsm[];
     double(*s)[kT + 1] = (double(*)[kT + 1])dsm;                    // tile -> L
     double(*x)[kT + 1] = (double(*)[kT + 1])(dsm + kT * (kT + 1));  // X = L^-1
+    __shared__ double rinv[kT];  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
+    __shared__ int bad;
     const int b = blockIdx.y;
     if (info[b]) return;
     double *blk = a + (int64_t)b * n * n;
     const int64_t o = (int64_t)k * kT;
     const int m = (int)(n - o < kT ? n - o : kT);
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
     // rows/columns past the block factor as the identity; X starts as I
     for (int e = t; e < kT * kT; e += kDiagThreads) {
         const int rr = e >> 6, c = e & 63;
         s[rr][c] = (rr < m && c < m) ? blk[(o + rr) * n + o + c] : (rr == c ? 1.0 : 0.0);
         x[rr][c] = rr == c ? 1.0 : 0.0;
     }
-    // this thread's triangle elements (r, l), l <= r (r = -1: none)
-    constexpr int kPer = (kTri + kDiagThreads - 1) / kDiagThreads;  // 3
-    int er[kPer], el[kPer];
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const int e = t + q * kDiagThreads;
-        if (e < kTri) {
-            int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-            while (r * (r + 1) / 2 > e) --r;
-            while ((r + 1) * (r + 2) / 2 <= e) ++r;
-            er[q] = r;
-            el[q] = e - r * (r + 1) / 2;
-        } else {
-            er[q] = -1;
-            el[q] = 0;
-        }
-    }
-    __shared__ double rinv[kT];  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
-    __shared__ int bad;
     if (t == 0) bad = 0;
     __syncthreads();
     for (int j = 0; j < kT; ++j) {
@@ -150,26 +132,30 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
         __syncthreads();
         if (bad) break;
         if (t > j && t < kT) s[t][j] *= rinv[j];
+        if (t <= j) x[j][t] *= rinv[j];
         __syncthreads();
+        if (4 * w + 3 > j) {  // warp-uniform
 #pragma unroll
-        for (int q = 0; q < kPer; ++q)
-            if (el[q] > j) s[er[q]][el[q]] -= s[er[q]][j] * s[el[q]][j];
+            for (int q = 0; q < 4; ++q) {
+                const int r = 4 * w + q;
+                if (r <= j) continue;
+                const double lrj = s[r][j];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int l = lane + 32 * h;
+                    if (l > j) {
+                        if (l <= r) s[r][l] -= lrj * s[l][j];
+                    } else {
+                        x[r][l] -= lrj * x[j][l];
+                    }
+                }
+            }
+        }
         __syncthreads();
     }
     if (bad) {
         if (t == 0) info[b] = (int)(o + bad);  // LAPACK info: order of the failing minor
         return;
-    }
-    // L X = I, right-looking: row j of X scaled by 1 / L[j][j], then subtracted
-    // from the rows below; the columns c <= j of X are the only nonzero ones
-    for (int j = 0; j < kT; ++j) {
-        if (t <= j) x[j][t] *= rinv[j];
-        __syncthreads();
-        for (int e = t; e < (kT - 1 - j) * (j + 1); e += kDiagThreads) {
-            const int r = j + 1 + e / (j + 1), c = e % (j + 1);
-            x[r][c] -= s[r][j] * x[j][c];
-        }
-        __syncthreads();
     }
     for (int e = t; e < kT * kT; e += kDiagThreads) {
         const int rr = e >> 6, c = e & 63;
@@ -526,13 +512,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
             e = cudaFuncSetAttribute(chol_update<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(chol_diag<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kDiagSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(chol_diag<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kDiagSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(chol_diag<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kDiagSmem);
         if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch attributes: %s", cudaGetErrorString(e));
         done.fetch_or(1ull << (dev & 63));
@@ -560,7 +540,6 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                                                                     j_lo, j_hi, (int)batch, info);
     };
     const int cap_all = 1 << 30, cap_bulk = nsm * bulk_per_sm;
-    const int diag_threads = tune_knob("SFB_CHOL_DIAG_THREADS", 512);
     // Look-ahead: after super-panel i is factored, its update of the next
     // super-panel's columns (a_i) runs on the caller's stream, the bulk update
     // of everything beyond (b_i) on a second stream, where it overlaps the
@@ -590,15 +569,8 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     for (int p0 = 0; p0 < nt && e == cudaSuccess; p0 += W) {
         const int p1 = std::min(p0 + W, nt), p2 = std::min(p1 + W, nt);
         for (int k = p0; k < p1; ++k) {
-            if (diag_threads == 256)
-                chol_diag<256><<<dim3(1, (unsigned)batch), 256, kDiagSmem, st>>>(d_lmat, n, k, info,
-                                                                                 linv);
-            else if (diag_threads == 512)
-                chol_diag<512><<<dim3(1, (unsigned)batch), 512, kDiagSmem, st>>>(d_lmat, n, k, info,
-                                                                                 linv);
-            else
-                chol_diag<1024><<<dim3(1, (unsigned)batch), 1024, kDiagSmem, st>>>(d_lmat, n, k,
-                                                                                   info, linv);
+            chol_diag<<<dim3(1, (unsigned)batch), kDiagThreads, kDiagSmem, st>>>(d_lmat, n, k, info,
+                                                                            linv);
             if (k + 1 < nt)
                 chol_trsm<<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads, smem, st>>>(
                     d_lmat, n, k, info, linv);

@@ -492,7 +492,8 @@ static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, co
     std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
     auto hm = std::make_shared<HostMemo>();
     build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
-                   kMemoMaxWords, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0);
+                   kMemoMaxWords, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0,
+                   tune_knob("SFB_MEMO_RMAX_X10", 45) / 10.0);
     std::lock_guard<std::mutex> g(mc.mu);
     MemoEntry *victim = &mc.e[0];
     for (MemoEntry &en : mc.e)
