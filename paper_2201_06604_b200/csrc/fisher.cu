@@ -558,7 +558,10 @@ static int launch_fixed(int nr, int nc, unsigned blocks, size_t smem, cudaStream
         case 0x33: return launch_k<true, 4, W, JUMPS, 3, 3>(blocks, smem, st, a, j);
         case 0x34: return launch_k<true, 4, W, JUMPS, 3, 4>(blocks, smem, st, a, j);
         case 0x43: return launch_k<true, 4, W, JUMPS, 4, 3>(blocks, smem, st, a, j);
-        case 0x44: return launch_k<true, 4, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
+        case 0x44:
+            if (tune_knob("SFB_FISHER_FIXED_MINB", 4) == 3)  // tuning
+                return launch_k<true, 3, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
+            return launch_k<true, 4, W, JUMPS, 4, 4>(blocks, smem, st, a, j);
         default: return -1;
     }
 }
@@ -639,7 +642,9 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
         const int64_t target = 148LL * 2048 * 2 * q_knob / 4;
         nchunks = std::min<int64_t>({(int64_t)kMaxChunksLarge, reps, ceil_div(target, nloc)});
     } else {
-        const int64_t resident = (int64_t)sm_count() * 4 * kFisherThreads;
+        const int64_t resident = (int64_t)sm_count() *
+                                 (nr == 4 && nc == 4 ? tune_knob("SFB_FISHER_FIXED_MINB", 4) : 4) *
+                                 kFisherThreads;
         double best = 0;
         for (int64_t c = 1; c <= std::min<int64_t>(kMaxChunksLarge, reps); ++c) {
             const int64_t r = ceil_div(reps, c);
