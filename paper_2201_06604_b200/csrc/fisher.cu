@@ -220,6 +220,27 @@ __global__ void __launch_bounds__(256) advance_states_kernel(int64_t *cur, int64
     store_state(cur + 6 * w, s);
 }
 
+// out-of-place form (the host-state call: the final states are computed from
+// the start states next to the sampling kernel, and their download overlaps it)
+__global__ void __launch_bounds__(256) advance_states_out(const int64_t *cur, int64_t *out,
+                                                          int64_t lo, int64_t hi, const Jump jump) {
+    const int64_t w = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= hi) return;
+    Mrg s = load_state(cur + 6 * w);
+    apply(jump, s);
+    store_state(out + 6 * (w - lo), s);
+}
+
+// Side advance of a host-state call: when the launch is chunked, the final
+// states are produced by advance_states_out on `side` into `out` (after the
+// event `ready`, i.e. the state upload) instead of in place; `done` reports it.
+struct SideAdvance {
+    cudaStream_t side;
+    cudaEvent_t ready;
+    int64_t *out;
+    bool done;
+};
+
 // jw_global: column work for tables too wide for shared memory (else null)
 __global__ void rcont2_kernel(const int32_t *rowm, const int32_t *colm, int nr, int nc, int ntot,
                               const double *lf, int64_t *state, int64_t *mat, int *jw_global) {
@@ -592,11 +613,31 @@ using namespace sfb;
 
 extern "C" {
 
+static int fisher_replicates_impl(int64_t *d_cur, int64_t n_streams, const int64_t *nrowt, int nr,
+                                  const int64_t *ncolt, int nc, const double *lf, int64_t lf_len,
+                                  double threshold, int64_t reps, int64_t item_lo,
+                                  int64_t item_hi, double *d_stats, int64_t *d_item_counts,
+                                  uint64_t *d_count, int zero_count, void *stream,
+                                  SideAdvance *side);
+
 int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrowt, int nr,
                           const int64_t *ncolt, int nc, const double *lf, int64_t lf_len,
                           double threshold, int64_t reps, int64_t item_lo, int64_t item_hi,
                           double *d_stats, int64_t *d_item_counts, uint64_t *d_count,
                           int zero_count, void *stream) {
+    return fisher_replicates_impl(d_cur, n_streams, nrowt, nr, ncolt, nc, lf, lf_len, threshold,
+                                  reps, item_lo, item_hi, d_stats, d_item_counts, d_count,
+                                  zero_count, stream, nullptr);
+}
+
+}  // extern "C"
+
+static int fisher_replicates_impl(int64_t *d_cur, int64_t n_streams, const int64_t *nrowt, int nr,
+                                  const int64_t *ncolt, int nc, const double *lf, int64_t lf_len,
+                                  double threshold, int64_t reps, int64_t item_lo,
+                                  int64_t item_hi, double *d_stats, int64_t *d_item_counts,
+                                  uint64_t *d_count, int zero_count, void *stream,
+                                  SideAdvance *side) {
     int ntot = 0;
     if (int rc = check_margins(nrowt, nr, ncolt, nc, lf, lf_len, &ntot)) return rc;
     if (reps < 0) return fail(SFB_E_INVALID_ARGUMENT, "reps must be >= 0");
@@ -743,6 +784,25 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     const int minb = tune_knob("SFB_FISHER_MINB", 4);
     const bool fixed_ok = lf_smem && minb >= 4 && tune_knob("SFB_FISHER_FIXED", 1) &&
                           tune_knob("SFB_FISHER_WALK", kFisherWalkDefault) == kFisherWalkDefault;
+    // host-state calls: the final states from the start states on the side
+    // stream, enqueued first so the download overlaps the sampling kernel
+    const bool side_adv = side && nchunks > 1 && nloc > 0;
+    if (side_adv) {
+        thread_local Jump total;
+        thread_local uint64_t total_n = ~0ull;
+        if (total_n != (uint64_t)reps * (uint64_t)F) {
+            jump_pow((uint64_t)reps * (uint64_t)F, &total);
+            total_n = (uint64_t)reps * (uint64_t)F;
+        }
+        e = cudaStreamWaitEvent(side->side, side->ready, 0);
+        if (e == cudaSuccess) {
+            advance_states_out<<<(unsigned)ceil_div(nloc, 256), 256, 0, side->side>>>(
+                d_cur, side->out, item_lo, item_hi, total);
+            e = cudaGetLastError();
+        }
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher side advance: %s", cudaGetErrorString(e));
+        side->done = true;
+    }
     int fx = -1;
     if (!wide && fixed_ok)
         fx = large ? launch_fixed(nr, nc, blocks, smem, st, a, jl)
@@ -772,7 +832,7 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
             e = launch_fisher<false, 1>(blocks, smem, st, a, jumps);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
-    if (e == cudaSuccess && nchunks > 1) {
+    if (e == cudaSuccess && nchunks > 1 && !side_adv) {
         thread_local Jump total;
         thread_local uint64_t total_n = ~0ull;
         if (total_n != (uint64_t)reps * (uint64_t)F) {
@@ -788,6 +848,8 @@ int sfb_fisher_replicates(int64_t *d_cur, int64_t n_streams, const int64_t *nrow
     return SFB_OK;
 }
 
+extern "C" {
+
 // Host-buffer form of sfb_fisher_replicates: the call a host-authoritative
 // fisher_sim makes (fisher.py:147-157 with states, count and statistics in
 // host memory).  Synchronous, like the reference's kernel call: uploads the
@@ -799,6 +861,8 @@ struct HostCallScratch {
     std::mutex mu;
     unsigned char *dev = nullptr;
     size_t cap = 0;
+    cudaStream_t side = nullptr;  // final-state advance + download (SideAdvance)
+    cudaEvent_t ev_up = nullptr, ev_down = nullptr;
 };
 
 int sfb_fisher_replicates_host(int64_t *h_cur, int64_t n_streams, const int64_t *nrowt, int nr,
@@ -820,7 +884,8 @@ int sfb_fisher_replicates_host(int64_t *h_cur, int64_t n_streams, const int64_t 
     const int64_t nloc = item_hi - item_lo;
     const size_t state_bytes = (size_t)nloc * 48;
     const size_t stats_bytes = h_stats ? (size_t)nloc * (size_t)reps * 8 : 0;
-    const size_t need = 256 + ((state_bytes + 255) & ~(size_t)255) + stats_bytes;
+    const size_t state_pad = (state_bytes + 255) & ~(size_t)255;
+    const size_t need = 256 + 2 * state_pad + stats_bytes;  // count | start | final | stats
     cudaError_t e = cudaSuccess;
     if (need > sc.cap) {
         if (sc.dev) {
@@ -836,20 +901,34 @@ int sfb_fisher_replicates_host(int64_t *h_cur, int64_t n_streams, const int64_t 
         }
         sc.cap = need;
     }
+    if (!sc.side) {
+        e = cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc.ev_up, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sc.ev_down, cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher side stream: %s", cudaGetErrorString(e));
+    }
     uint64_t *d_count = (uint64_t *)sc.dev;
     int64_t *d_rows = (int64_t *)(sc.dev + 256);
-    double *d_stats = h_stats ? (double *)(sc.dev + 256 + ((state_bytes + 255) & ~(size_t)255))
-                              : nullptr;
+    int64_t *d_final = (int64_t *)(sc.dev + 256 + state_pad);
+    double *d_stats = h_stats ? (double *)(sc.dev + 256 + 2 * state_pad) : nullptr;
     if (nloc)
         e = cudaMemcpyAsync(d_rows, h_cur + 6 * item_lo, state_bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventRecord(sc.ev_up, st);
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "state upload: %s", cudaGetErrorString(e));
+    SideAdvance side{sc.side, sc.ev_up, d_final, false};
     // the kernel addresses stream w at cur + 6 w: rebase so row item_lo is d_rows[0]
-    if (int rc = sfb_fisher_replicates(d_rows - 6 * item_lo, n_streams, nrowt, nr, ncolt, nc, lf,
-                                       lf_len, threshold, reps, item_lo, item_hi, d_stats, nullptr,
-                                       d_count, 1, stream))
+    if (int rc = fisher_replicates_impl(d_rows - 6 * item_lo, n_streams, nrowt, nr, ncolt, nc, lf,
+                                        lf_len, threshold, reps, item_lo, item_hi, d_stats,
+                                        nullptr, d_count, 1, stream, &side))
         return rc;
-    if (nloc)
+    if (side.done) {  // final states downloaded on the side stream, next to the kernel
+        e = cudaMemcpyAsync(h_cur + 6 * item_lo, d_final, state_bytes, cudaMemcpyDeviceToHost,
+                            sc.side);
+        if (e == cudaSuccess) e = cudaEventRecord(sc.ev_down, sc.side);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, sc.ev_down, 0);
+    } else if (nloc) {
         e = cudaMemcpyAsync(h_cur + 6 * item_lo, d_rows, state_bytes, cudaMemcpyDeviceToHost, st);
+    }
     if (e == cudaSuccess && stats_bytes)
         e = cudaMemcpyAsync(h_stats, d_stats, stats_bytes, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess)
