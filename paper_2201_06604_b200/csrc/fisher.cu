@@ -211,8 +211,12 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
 // item's chunks all read its start state, and nothing orders thread blocks);
 // afterwards every item advances by exactly reps * (I-1)(J-1) draws (one
 // uniform per free cell, _kernels.py:210-212), J = A^(reps F), in this kernel.
+// Launched as a programmatic dependent of the sampling kernel (its launch
+// overlaps that kernel's tail); it must not touch a state before the
+// sampling kernel has completed, hence the grid-dependency wait first.
 __global__ void __launch_bounds__(256) advance_states_kernel(int64_t *cur, int64_t lo, int64_t hi,
                                                              const Jump jump) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t w = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= hi) return;
     Mrg s = load_state(cur + 6 * w);
@@ -839,9 +843,17 @@ static int fisher_replicates_impl(int64_t *d_cur, int64_t n_streams, const int64
             jump_pow((uint64_t)reps * (uint64_t)F, &total);
             total_n = (uint64_t)reps * (uint64_t)F;
         }
-        advance_states_kernel<<<(unsigned)ceil_div(nloc, 256), 256, 0, st>>>(d_cur, item_lo,
-                                                                             item_hi, total);
-        e = cudaGetLastError();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)ceil_div(nloc, 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed =
+            tune_knob("SFB_FISHER_PDL", 1) ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, advance_states_kernel, d_cur, item_lo, item_hi, total);
     }
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "fisher kernel launch: %s", cudaGetErrorString(e));
     in.done(st);
