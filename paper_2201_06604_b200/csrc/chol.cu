@@ -470,7 +470,8 @@ static void release(Scratch &sc, cudaStream_t st) {
 struct LookAhead {
     std::mutex mu;
     cudaStream_t sb = nullptr, sh = nullptr;  // bulk update (low priority), chain (high)
-    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s = nullptr;
+    cudaStream_t sr = nullptr;                // super-panel-local updates beside the chain
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s = nullptr, ev_h = nullptr, ev_r = nullptr;
 };
 
 static LookAhead &look_ahead(int dev) {
@@ -540,6 +541,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                                                                     j_lo, j_hi, (int)batch, info);
     };
     const int cap_all = 1 << 30, cap_bulk = nsm * bulk_per_sm;
+    const bool split = tune_knob("SFB_CHOL_SPLIT", 1) != 0;
     // Look-ahead: after super-panel i is factored, its update of the next
     // super-panel's columns (a_i) runs on the caller's stream, the bulk update
     // of everything beyond (b_i) on a second stream, where it overlaps the
@@ -559,6 +561,9 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_a, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_b, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_s, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&la.sr, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_h, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_r, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch streams: %s", cudaGetErrorString(e));
     }
     const cudaStream_t caller = st;
@@ -568,14 +573,35 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     bool pending_b = false;
     for (int p0 = 0; p0 < nt && e == cudaSuccess; p0 += W) {
         const int p1 = std::min(p0 + W, nt), p2 = std::min(p1 + W, nt);
+        // inside a super-panel the chain only waits for the update of the
+        // next column tile; the update of the super-panel's later columns runs
+        // on a third stream and is waited for one step later (the next
+        // column's own update touches the tiles it updated)
+        bool pending_r = false;
         for (int k = p0; k < p1; ++k) {
             chol_diag<<<dim3(1, (unsigned)batch), kDiagThreads, kDiagSmem, st>>>(d_lmat, n, k, info,
                                                                             linv);
             if (k + 1 < nt)
                 chol_trsm<<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads, smem, st>>>(
                     d_lmat, n, k, info, linv);
-            if (k + 1 < p1) update(st, k, k + 1, k + 1, p1, cap_all);
+            if (k + 1 < p1) {
+                if (split && k + 2 < p1) {
+                    cudaEventRecord(la.ev_h, st);  // panel k solved
+                    cudaStreamWaitEvent(la.sr, la.ev_h, 0);
+                }
+                if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);
+                if (split && k + 2 < p1) {
+                    update(st, k, k + 1, k + 1, k + 2, cap_all);       // column k+1: the chain
+                    update(la.sr, k, k + 1, k + 2, p1, cap_all);       // the rest, beside it
+                    cudaEventRecord(la.ev_r, la.sr);
+                    pending_r = true;
+                } else {
+                    update(st, k, k + 1, k + 1, p1, cap_all);
+                    pending_r = false;
+                }
+            }
         }
+        if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);
         if (p1 < nt) {
             cudaEventRecord(la.ev_a, st);  // super-panel p0 factored
             if (pending_b) cudaStreamWaitEvent(st, la.ev_b, 0);  // b of the previous super-panel
