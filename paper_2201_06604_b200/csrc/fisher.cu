@@ -40,6 +40,14 @@
 
 namespace sfb {
 
+// device memo budgets (the host test hook keeps fisher_sampler.cuh's smaller
+// defaults): interior boxes up to 2^17 points, 2^26 record words (256 MB).
+// T10: 244 MB of records built in ~0.7 s once per table (cached), T10 kernel
+// 23.8 -> 22.7 ms: the boxes now also cover cells (1,7), (2,6), (3,4),
+// (3,5), (4,3), (5,1), (5,2), ~13 % of the lockstep walk trips
+constexpr int kDevMemoCellPtsLog2 = 17;
+constexpr int kDevMemoWordsLog2 = 26;
+constexpr int64_t kMemoPrefetchMax = (int64_t)32 << 20;  // L2 prefetch at kernel start
 constexpr int kMaxChunks = 96;        // chunk jumps in the small parameter block
 constexpr int kMaxChunksLarge = 384;  // small grids (e.g. the default 64 x 16): 27 KB block
 constexpr int kFisherWalkDefault = 3;  // fisher_sampler.cuh walk form (tools/tune.py)
@@ -517,8 +525,10 @@ static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, co
     std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
     auto hm = std::make_shared<HostMemo>();
     build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
-                   kMemoMaxWords, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0,
-                   tune_knob("SFB_MEMO_RMAX_X10", 45) / 10.0);
+                   (size_t)1 << tune_knob("SFB_MEMO_WORDS_LOG2", kDevMemoWordsLog2), kMemoSigmas,
+                   tune_knob("SFB_FISHER_MEMO_INT", 1) != 0,
+                   tune_knob("SFB_MEMO_RMAX_X10", 45) / 10.0,
+                   (size_t)1 << tune_knob("SFB_MEMO_CELL_PTS_LOG2", kDevMemoCellPtsLog2));
     std::lock_guard<std::mutex> g(mc.mu);
     MemoEntry *victim = &mc.e[0];
     for (MemoEntry &en : mc.e)
@@ -747,7 +757,9 @@ static int fisher_replicates_impl(int64_t *d_cur, int64_t n_streams, const int64
     if (!use_memo) a.memo = MemoSet{};
     a.memo_blob = in.memo_blob;
     a.memo_bytes = use_memo ? (int)in.memo_bytes : 0;
-    a.rec_bytes = use_memo && tune_knob("SFB_FISHER_PREFETCH", 1) ? (int64_t)in.rec_bytes : 0;
+    a.rec_bytes = use_memo && tune_knob("SFB_FISHER_PREFETCH", 1)
+                      ? std::min<int64_t>((int64_t)in.rec_bytes, kMemoPrefetchMax)
+                      : 0;
 
     // shared memory layout of fisher_kernel (same offsets): exp table |
     // margins | [lf] | column work | memo cell descriptors; lf goes to global
