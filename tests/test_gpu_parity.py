@@ -959,3 +959,28 @@ def test_fisher_fixed_shapes_vs_oracle(shape, mode, monkeypatch):
         assert r.counts == ref["counts"]
         assert np.array_equal(r.statistics, ref["statistics"])
         assert np.array_equal(st.current, ref_st)
+
+
+@pytest.mark.parametrize("table_key,n,g", [("T4", 10**6, (256, 64)), ("T10", 200000, (64, 16)),
+                                           ("T4", 3000, (16, 16))])
+def test_fisher_host_and_device_states_agree(G, table_key, n, g):
+    """fisher_sim on host-authoritative states (one synchronous C-ABI call; for
+    chunked launches the final states are computed on a side stream and
+    downloaded while the sampling kernel runs) and on device-resident states
+    (in-stream advance) give the same counts and final states, and both match
+    the oracle's final states A^(reps F) s (fisher.py:118-164)."""
+    import torch
+
+    table = np.array(G[table_key])
+    a, b = fresh(g[0] * g[1]), fresh(g[0] * g[1])
+    _ = b.device_current()  # b starts device-resident
+    ra = sf.fisher_sim(table, n, a, grid=grid(g))
+    rb = sf.fisher_sim(table, n, b, grid=grid(g))
+    torch.cuda.synchronize()
+    assert ra.counts == rb.counts and ra.sim_num == rb.sim_num
+    assert np.array_equal(a.current, b.current)
+    f = (table.shape[0] - 1) * (table.shape[1] - 1)
+    reps = ra.sim_num // (g[0] * g[1])
+    seeds = oa.fresh_states(g[0] * g[1])
+    for w in (0, 1, g[0] * g[1] // 2, g[0] * g[1] - 1):
+        assert np.array_equal(a.current[w], orc.skip(seeds[w], reps * f)), w
