@@ -32,6 +32,7 @@
 #include <atomic>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "exp_glibc.cuh"
@@ -40,11 +41,14 @@
 
 namespace sfb {
 
-// device memo budgets (the host test hook keeps fisher_sampler.cuh's smaller
-// defaults): interior boxes up to 2^17 points, 2^26 record words (256 MB).
-// T10: 244 MB of records built in ~0.7 s once per table (cached), T10 kernel
-// 23.8 -> 22.7 ms: the boxes now also cover cells (1,7), (2,6), (3,4),
-// (3,5), (4,3), (5,1), (5,2), ~13 % of the lockstep walk trips
+// Device memo budgets.  Level 0 (the first use of a table) keeps
+// fisher_sampler.cuh's defaults: 2^15 points per interior box, 2^25 record
+// words, built in ~10-130 ms.  When a level-0 set was capped (cells left to
+// the walk) and the table is used again, a host thread builds level 1 in the
+// background -- 2^17 points, 2^26 words: T10 244 MB in ~0.7 s, T10 kernel
+// 23.8 -> 22.6 ms, month 5.88 -> 5.68 ms -- and the next call after it is
+// ready picks it up.  So a one-off call never waits for the large build and a
+// Monte Carlo loop over one table gets it after its first second.
 constexpr int kDevMemoCellPtsLog2 = 17;
 constexpr int kDevMemoWordsLog2 = 26;
 constexpr int64_t kMemoPrefetchMax = (int64_t)32 << 20;  // L2 prefetch at kernel start
@@ -496,6 +500,8 @@ struct MemoEntry {
     std::vector<double> lf;
     std::shared_ptr<const HostMemo> memo;
     uint64_t version = 0, tick = 0;
+    int level = 0;           // budget level of `memo` (see kDevMemoCellPtsLog2)
+    bool upgrading = false;  // a level-1 build is running
 };
 
 struct MemoCache {
@@ -504,39 +510,75 @@ struct MemoCache {
     uint64_t version = 0, tick = 0;
 };
 
+static std::shared_ptr<HostMemo> build_memo(const std::vector<int64_t> &key, int nr, int nc,
+                                            int ntot, const double *lf, int level) {
+    std::vector<int32_t> rowm(key.begin(), key.begin() + nr);
+    std::vector<int32_t> colm(key.begin() + nr + 1, key.begin() + nr + 1 + nc);
+    auto hm = std::make_shared<HostMemo>();
+    const int pts = level ? tune_knob("SFB_MEMO_CELL_PTS_LOG2", kDevMemoCellPtsLog2) : 15;
+    const int words = level ? tune_knob("SFB_MEMO_WORDS_LOG2", kDevMemoWordsLog2) : 25;
+    build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
+                   (size_t)1 << words, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0,
+                   tune_knob("SFB_MEMO_RMAX_X10", 45) / 10.0, (size_t)1 << pts);
+    return hm;
+}
+
+static MemoEntry *find_memo(MemoCache &mc, const std::vector<int64_t> &key, const double *lf,
+                            int64_t lf_len) {
+    for (MemoEntry &en : mc.e)
+        if (en.memo && en.margins == key && (int64_t)en.lf.size() == lf_len &&
+            memcmp(en.lf.data(), lf, (size_t)lf_len * 8) == 0)
+            return &en;
+    return nullptr;
+}
+
 static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, const int64_t *ncolt,
                                                 int nc, int ntot, const double *lf, int64_t lf_len,
                                                 uint64_t *version) {
-    static MemoCache mc;
+    // never destroyed: a background upgrade may still run at process exit
+    static MemoCache &mc = *new MemoCache;
     std::vector<int64_t> key(nrowt, nrowt + nr);
     key.push_back(-1);
     key.insert(key.end(), ncolt, ncolt + nc);
+    const int upgrade = tune_knob("SFB_FISHER_MEMO_UPGRADE", 1);  // 0 off, 2 synchronous
     {
         std::lock_guard<std::mutex> g(mc.mu);
-        for (MemoEntry &en : mc.e)
-            if (en.memo && en.margins == key && (int64_t)en.lf.size() == lf_len &&
-                memcmp(en.lf.data(), lf, (size_t)lf_len * 8) == 0) {
-                en.tick = ++mc.tick;
-                *version = en.version;
-                return en.memo;
+        if (MemoEntry *en = find_memo(mc, key, lf, lf_len)) {
+            en->tick = ++mc.tick;
+            *version = en->version;
+            if (upgrade == 1 && en->level == 0 && en->memo->capped && !en->upgrading) {
+                // second use of a capped table: the large set in the background
+                en->upgrading = true;
+                std::vector<double> lfv(lf, lf + lf_len);
+                std::thread([key, lfv, nr, nc, ntot] {
+                    std::shared_ptr<HostMemo> big = build_memo(key, nr, nc, ntot, lfv.data(), 1);
+                    std::lock_guard<std::mutex> g2(mc.mu);
+                    MemoEntry *cur = find_memo(mc, key, lfv.data(), (int64_t)lfv.size());
+                    if (cur && cur->level == 0) {
+                        cur->memo = big;
+                        cur->level = 1;
+                        cur->version = ++mc.version;  // input caches re-upload
+                    }
+                    if (cur) cur->upgrading = false;
+                }).detach();
             }
+            return en->memo;
+        }
     }
     // build outside the lock (other tables' calls proceed meanwhile)
-    std::vector<int32_t> rowm(nrowt, nrowt + nr), colm(ncolt, ncolt + nc);
-    auto hm = std::make_shared<HostMemo>();
-    build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
-                   (size_t)1 << tune_knob("SFB_MEMO_WORDS_LOG2", kDevMemoWordsLog2), kMemoSigmas,
-                   tune_knob("SFB_FISHER_MEMO_INT", 1) != 0,
-                   tune_knob("SFB_MEMO_RMAX_X10", 45) / 10.0,
-                   (size_t)1 << tune_knob("SFB_MEMO_CELL_PTS_LOG2", kDevMemoCellPtsLog2));
+    const int level = upgrade == 2 ? 1 : 0;
+    std::shared_ptr<HostMemo> hm = build_memo(key, nr, nc, ntot, lf, level);
     std::lock_guard<std::mutex> g(mc.mu);
     MemoEntry *victim = &mc.e[0];
     for (MemoEntry &en : mc.e)
-        if (!en.memo ? victim->memo != nullptr : (victim->memo && en.tick < victim->tick))
+        if (!en.upgrading &&
+            (!en.memo ? victim->memo != nullptr : (victim->memo && en.tick < victim->tick)))
             victim = &en;
     victim->margins = std::move(key);
     victim->lf.assign(lf, lf + lf_len);
     victim->memo = hm;
+    victim->level = level;
+    victim->upgrading = false;
     victim->version = ++mc.version;
     victim->tick = ++mc.tick;
     *version = victim->version;
