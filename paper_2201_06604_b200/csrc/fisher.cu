@@ -543,7 +543,8 @@ static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, co
     const int upgrade = tune_knob("SFB_FISHER_MEMO_UPGRADE", 1);  // 0 off, 2 synchronous
     {
         std::lock_guard<std::mutex> g(mc.mu);
-        if (MemoEntry *en = find_memo(mc, key, lf, lf_len)) {
+        MemoEntry *en = find_memo(mc, key, lf, lf_len);
+        if (en && !(upgrade == 2 && en->level == 0)) {
             en->tick = ++mc.tick;
             *version = en->version;
             if (upgrade == 1 && en->level == 0 && en->memo->capped && !en->upgrading) {
@@ -569,16 +570,25 @@ static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, co
     const int level = upgrade == 2 ? 1 : 0;
     std::shared_ptr<HostMemo> hm = build_memo(key, nr, nc, ntot, lf, level);
     std::lock_guard<std::mutex> g(mc.mu);
-    MemoEntry *victim = &mc.e[0];
-    for (MemoEntry &en : mc.e)
-        if (!en.upgrading &&
-            (!en.memo ? victim->memo != nullptr : (victim->memo && en.tick < victim->tick)))
-            victim = &en;
+    // the same table built meanwhile (or a level-0 entry being replaced): reuse its slot
+    MemoEntry *victim = find_memo(mc, key, lf, lf_len);
+    const bool same = victim != nullptr;
+    if (!same) {
+        victim = &mc.e[0];
+        for (MemoEntry &en : mc.e)
+            if (!en.upgrading &&
+                (!en.memo ? victim->memo != nullptr : (victim->memo && en.tick < victim->tick)))
+                victim = &en;
+    } else if (victim->level > level) {  // a larger set landed while this one was built
+        victim->tick = ++mc.tick;
+        *version = victim->version;
+        return victim->memo;
+    }
     victim->margins = std::move(key);
     victim->lf.assign(lf, lf + lf_len);
     victim->memo = hm;
     victim->level = level;
-    victim->upgrading = false;
+    if (!same) victim->upgrading = false;  // a running upgrade of this table keeps its flag
     victim->version = ++mc.version;
     victim->tick = ++mc.tick;
     *version = victim->version;

@@ -658,7 +658,9 @@ int sfb_host_fisher_replicates(int64_t *cur, const int64_t *nrowt, int nr, const
     const bool use_memo = tune_knob("SFB_FISHER_MEMO", 1) != 0;
     if (use_memo)
         build_memo_set(rowm.data(), nr, colm.data(), nc, (int)ntot, LfPlain{lf}, kExpTable, hm,
-                       kMemoMaxWords, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0);
+                       (size_t)1 << tune_knob("SFB_MEMO_WORDS_LOG2", 25), kMemoSigmas,
+                       tune_knob("SFB_FISHER_MEMO_INT", 1) != 0, kMemoIntRadiusMax,
+                       (size_t)1 << tune_knob("SFB_MEMO_CELL_PTS_LOG2", 15));
     const MemoSet mp = use_memo ? hm.view() : MemoSet{};
     const int walk = tune_knob("SFB_FISHER_WALK", 3);
     int64_t hits = 0;

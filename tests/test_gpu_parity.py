@@ -984,3 +984,20 @@ def test_fisher_host_and_device_states_agree(G, table_key, n, g):
     seeds = oa.fresh_states(g[0] * g[1])
     for w in (0, 1, g[0] * g[1] // 2, g[0] * g[1] - 1):
         assert np.array_equal(a.current[w], orc.skip(seeds[w], reps * f)), w
+
+
+def test_fisher_large_memo_level_bit_exact(G, A, monkeypatch):
+    """The large memo set (SFB_FISHER_MEMO_UPGRADE=2: built synchronously at
+    the first use, with the budgets the background upgrade uses) gives the
+    golden counts, statistics and states bit for bit."""
+    monkeypatch.setenv("SFB_FISHER_MEMO_UPGRADE", "2")
+    tabs = _tables(G, A)
+    for key in ("F_T10_1e6", "F_month_s", "F_Ebig"):
+        g = G[key]
+        st = fresh(g["n_streams"])
+        want = key + "_stats" in A
+        r = sf.fisher_sim(tabs[g["table"]], g["n"], st, grid=grid(g["grid"]), return_stats=want)
+        assert r.counts == g["counts"]
+        assert sha(st.current) == g["states_sha"]
+        if want:
+            assert np.array_equal(r.statistics, A[key + "_stats"])
