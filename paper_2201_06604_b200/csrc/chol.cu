@@ -49,16 +49,6 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// rows [r0, r0 + rows) x 64 columns at column c0 of block `blk` (pitch n) into
-// shared s[64][kPitch]; rows past `rows` are zero
-__device__ __forceinline__ void load_tile(double *s, const double *blk, int64_t n, int64_t r0,
-                                          int rows, int64_t c0, int cols) {
-    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
-        const int r = e >> 6, c = e & 63;
-        s[r * kPitch + c] = (r < rows && c < cols) ? blk[(r0 + r) * n + c0 + c] : 0.0;
-    }
-}
-
 // acc (this warp's 32 x 32 quarter of a 64 x 64 tile, 4 x 4 DMMA tiles of
 // 8 x 8, two doubles per lane each) = sa[0:64, 0:64] * sb[0:64, 0:64]^T
 __device__ __forceinline__ void tile_product(const double *sa, const double *sb,
@@ -85,24 +75,110 @@ __device__ __forceinline__ void tile_product(const double *sa, const double *sb,
 }
 
 // Factor tile (k, k) of every block and store the inverse of its lower factor.
-// The tile's factorisation is on the critical path of every panel step.  512
-// threads: warp w owns rows 4w .. 4w + 3, lane l columns l and l + 32.  Step j
-// is three barriers long: the owner of row j takes the square root and its
-// reciprocal; column j is scaled; then every row r > j updates its trailing
-// part (columns j < l <= r) and, in the same pass, row r of X = L^-1 (L X = I
-// right-looking: columns l <= j, X's row j final) -- warps whose rows all lie
-// above j skip the pass.  Loops stay rolled: unrolled register-resident forms
-// are tens of thousands of straight-line instructions and stalled on
-// instruction fetch (measured 113-200 us per tile).
-constexpr int kDiagThreads = 512;
-constexpr int kDiagSmem = 2 * kT * (kT + 1) * (int)sizeof(double);
+// The tile's factorisation is on the critical path of every panel step, so it
+// is blocked in 16-column steps to keep the number of block-wide barriers
+// small (~20 instead of 3 per column):
+//   (a) warp 0 factors the 16 x 16 diagonal block in registers (lane i holds
+//       row i; the column is broadcast with shuffles, no barriers);
+//   (b) the rows below solve against it (one thread per row, forward
+//       substitution in registers);
+//   (c) the trailing lower part is updated (thread (rr, cc) of every 16 x 16
+//       sub-block, the sub-blocks' row/column values loaded once per column);
+// then the inverse X = L^-1: the four diagonal blocks by forward substitution
+// (warp p, lane c = column c of X_pp), the off-diagonal blocks in three stages
+// X_ip = -X_ii sum_{p <= m < i} L_im X_mp.  (Unblocked 64-step forms with
+// three barriers per column measured 50-60 us per tile under ncu;
+// register-resident fully unrolled 64-column forms stalled on instruction
+// fetch, 113-200 us.)
+constexpr int kDiagThreads = 256;
+constexpr int kDP = kT + 1;  // shared pitch (column accesses conflict-free)
+constexpr int kDiagSmem = (2 * kT * kDP + 3 * 256 + kT) * (int)sizeof(double);
+
+// sqrt(d) and 1/sqrt(d) for d > 0 without the library's out-of-line slow paths
+// (their calls made the unrolled factor loop save its row registers to the
+// stack): rsqrt.approx seed, two Newton steps, a residual-corrected root;
+// within a few ulp of LAPACK's sqrt and 1/sqrt (tolerance-level parity).
+// Subnormal-range d is scaled by 2^600 first (the seed flushes subnormals).
+__device__ __forceinline__ void sqrt_rsqrt(double d, double &l, double &r) {
+    const bool tiny = d < 0x1p-900;
+    const double ds = tiny ? d * 0x1p600 : d;
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(ds));
+    const double h = 0.5 * ds;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    double x = ds * y;
+    x = fma(0.5 * y, fma(-x, x, ds), x);
+    l = tiny ? x * 0x1p-300 : x;
+    r = tiny ? y * 0x1p300 : y;
+}
+
+// (a): warp 0, lanes 0..15 own rows; returns 0 or the 1-based failing column
+__device__ __forceinline__ int factor16(double (*s)[kDP], double *rinv, int p0, int lane) {
+    const int i = lane & 15;
+    double v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = s[p0 + i][p0 + c];  // c > i: never read
+    int fail = 0;  // no early exit: the loop stays unrolled (v in registers)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const double d = __shfl_sync(0xffffffffu, v[j], j);
+        if (!(d > 0.0) && !fail) fail = j + 1;  // warp-uniform
+        double l, r;
+        sqrt_rsqrt(d, l, r);
+        const double sc = v[j] * r;
+        v[j] = i == j ? l : (i > j ? sc : v[j]);
+        if (lane == j) rinv[p0 + j] = r;
+#pragma unroll
+        for (int c = 1; c < 16; ++c) {  // constant trip count: unrolled before the j loop
+            if (c > j) {
+                const double lc = __shfl_sync(0xffffffffu, v[j], c);
+                if (i >= c) v[c] -= v[j] * lc;
+            }
+        }
+    }
+    if (lane < 16 && !fail) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) s[p0 + i][p0 + c] = v[c];  // c > i: unchanged values
+    }
+    return fail;
+}
+
+// (c): rows/columns [r0, 64) lower part -= A[:, p0:p0+16] A[:, p0:p0+16]^T,
+// NB = (64 - r0) / 16 sub-blocks per side
+template <int NB>
+__device__ __forceinline__ void trailing16(double (*s)[kDP], int p0, int r0, int t) {
+    const int rr = t >> 4, cc = t & 15;
+    double acc[NB][NB];
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+        for (int bj = 0; bj < NB; ++bj) acc[bi][bj] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        double rv[NB], cv[NB];
+#pragma unroll
+        for (int bi = 0; bi < NB; ++bi) rv[bi] = s[r0 + 16 * bi + rr][p0 + c];
+#pragma unroll
+        for (int bj = 0; bj < NB; ++bj) cv[bj] = s[r0 + 16 * bj + cc][p0 + c];
+#pragma unroll
+        for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+            for (int bj = 0; bj <= bi; ++bj) acc[bi][bj] += rv[bi] * cv[bj];
+    }
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+        for (int bj = 0; bj <= bi; ++bj) s[r0 + 16 * bi + rr][r0 + 16 * bj + cc] -= acc[bi][bj];
+}
 
 __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, int k, int *info,
                                                           double *linv) {
     extern __shared__ double dsm[];
-    double(*s)[kT + 1] = (double(*)[kT + 1])dsm;                    // tile -> L
-    double(*x)[kT + 1] = (double(*)[kT + 1])(dsm + kT * (kT + 1));  // X = L^-1
-    __shared__ double rinv[kT];  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
+    double(*s)[kDP] = (double(*)[kDP])dsm;                // tile -> L
+    double(*x)[kDP] = (double(*)[kDP])(dsm + kT * kDP);   // X = L^-1
+    double *tmp = dsm + 2 * kT * kDP;                     // stage products, 3 x 16 x 16
+    double *rinv = tmp + 3 * 256;  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
     __shared__ int bad;
     const int b = blockIdx.y;
     if (info[b]) return;
@@ -110,52 +186,93 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
     const int64_t o = (int64_t)k * kT;
     const int m = (int)(n - o < kT ? n - o : kT);
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-    // rows/columns past the block factor as the identity; X starts as I
-    for (int e = t; e < kT * kT; e += kDiagThreads) {
-        const int rr = e >> 6, c = e & 63;
-        s[rr][c] = (rr < m && c < m) ? blk[(o + rr) * n + o + c] : (rr == c ? 1.0 : 0.0);
-        x[rr][c] = rr == c ? 1.0 : 0.0;
+    // rows/columns past the block factor as the identity; X starts as 0.
+    // Every load in flight before the first shared store.
+    {
+        constexpr int kPer = kT * kT / kDiagThreads;
+        double v[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = t + q * kDiagThreads, rr = e >> 6, c = e & 63;
+            v[q] = (rr < m && c < m) ? blk[(o + rr) * n + o + c] : (rr == c ? 1.0 : 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = t + q * kDiagThreads, rr = e >> 6, c = e & 63;
+            s[rr][c] = v[q];
+            x[rr][c] = 0.0;
+        }
     }
     if (t == 0) bad = 0;
     __syncthreads();
-    for (int j = 0; j < kT; ++j) {
-        if (t == j) {
-            const double d = s[j][j];
-            if (!(d > 0.0)) {
-                bad = j + 1;
-            } else {
-                const double ljj = sqrt(d);
-                s[j][j] = ljj;
-                rinv[j] = 1.0 / ljj;
-            }
+    for (int p = 0; p < 4; ++p) {
+        const int p0 = 16 * p, r0 = p0 + 16;
+        if (w == 0) {
+            const int f = factor16(s, rinv, p0, lane);
+            if (f && lane == 0) bad = p0 + f;
         }
         __syncthreads();
         if (bad) break;
-        if (t > j && t < kT) s[t][j] *= rinv[j];
-        if (t <= j) x[j][t] *= rinv[j];
-        __syncthreads();
-        if (4 * w + 3 > j) {  // warp-uniform
+        if (p == 3) break;
+        if (t < kT - r0) {  // (b) row r0 + t of the panel: Y L_pp^T = A
+            const int r = r0 + t;
+            double y[16];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int r = 4 * w + q;
-                if (r <= j) continue;
-                const double lrj = s[r][j];
+            for (int c = 0; c < 16; ++c) y[c] = s[r][p0 + c];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int l = lane + 32 * h;
-                    if (l > j) {
-                        if (l <= r) s[r][l] -= lrj * s[l][j];
-                    } else {
-                        x[r][l] -= lrj * x[j][l];
-                    }
-                }
+            for (int c = 0; c < 16; ++c) {
+                y[c] *= rinv[p0 + c];
+#pragma unroll
+                for (int q = c + 1; q < 16; ++q) y[q] -= y[c] * s[p0 + q][p0 + c];
             }
+#pragma unroll
+            for (int c = 0; c < 16; ++c) s[r][p0 + c] = y[c];
         }
+        __syncthreads();
+        if (p == 0) trailing16<3>(s, p0, r0, t);
+        else if (p == 1) trailing16<2>(s, p0, r0, t);
+        else trailing16<1>(s, p0, r0, t);
         __syncthreads();
     }
     if (bad) {
         if (t == 0) info[b] = (int)(o + bad);  // LAPACK info: order of the failing minor
         return;
+    }
+    // X_pp = L_pp^-1: warp p, lane c computes column c (L X = I, right-looking)
+    if (w < 4 && lane < 16) {
+        const int p0 = 16 * w, c = lane;
+        double xv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xv[i] = i == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            xv[i] *= rinv[p0 + i];
+#pragma unroll
+            for (int q = i + 1; q < 16; ++q) xv[q] -= s[p0 + q][p0 + i] * xv[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[p0 + i][p0 + c] = xv[i];
+    }
+    __syncthreads();
+    // X_ip = -X_ii sum_{p <= q < i} L_iq X_qp, by distance d = i - p
+    for (int d = 1; d < 4; ++d) {
+        const int nblk = 4 - d;
+        for (int e = t; e < nblk * 256; e += kDiagThreads) {
+            const int p = e >> 8, rr = (e >> 4) & 15, c = e & 15, i = p + d;
+            double acc = 0.0;
+#pragma unroll 16
+            for (int q = 16 * p; q < 16 * i; ++q) acc += s[16 * i + rr][q] * x[q][16 * p + c];
+            tmp[e] = acc;
+        }
+        __syncthreads();
+        for (int e = t; e < nblk * 256; e += kDiagThreads) {
+            const int p = e >> 8, rr = (e >> 4) & 15, c = e & 15, i = p + d;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc += x[16 * i + rr][16 * i + q] * tmp[p * 256 + q * 16 + c];
+            x[16 * i + rr][16 * p + c] = -acc;
+        }
+        __syncthreads();
     }
     for (int e = t; e < kT * kT; e += kDiagThreads) {
         const int rr = e >> 6, c = e & 63;
@@ -176,10 +293,25 @@ __global__ void __launch_bounds__(kGemmThreads) chol_trsm(double *a, int64_t n, 
     const int64_t I = (int64_t)k + 1 + blockIdx.x;
     const int64_t r0 = I * kT, c0 = (int64_t)k * kT;
     const int rows = (int)(n - r0 < kT ? n - r0 : kT);
-    load_tile(sa, blk, n, r0, rows, c0, kT);
     const double *li = linv + (int64_t)b * kT * kT;
-    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x)
-        sb[(e >> 6) * kPitch + (e & 63)] = li[e];
+    {
+        // every load of both tiles in flight before the first shared store
+        // (the loop form waited on one global round trip per few elements)
+        constexpr int kPer = kT * kT / kGemmThreads;
+        double va[kPer], vb[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = threadIdx.x + q * kGemmThreads, rr = e >> 6, c = e & 63;
+            va[q] = rr < rows ? blk[(r0 + rr) * n + c0 + c] : 0.0;
+            vb[q] = li[e];
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = threadIdx.x + q * kGemmThreads, rr = e >> 6, c = e & 63;
+            sa[rr * kPitch + c] = va[q];
+            sb[rr * kPitch + c] = vb[q];
+        }
+    }
     __syncthreads();
     double acc[4][4][2];
     tile_product(sa, sb, acc);  // A_Ik Linv^T: B[q][c] = Linv[c][q]
