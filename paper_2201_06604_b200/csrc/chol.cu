@@ -11,9 +11,11 @@
 //     panel k, every launch covering all B blocks (grid.y = batch):
 //       chol_diag    -- factor tile (k, k) in shared memory (unblocked, rank-1
 //                       updates) and invert it (row-wise substitution);
-//       chol_trsm    -- panel tiles (I, k), I > k:  A_Ik <- A_Ik L_kk^-T as a
+//       chol_panel   -- panel tiles (I, k), I > k:  A_Ik <- A_Ik L_kk^-T as a
 //                       64 x 64 x 64 product with the inverse (the TRSM-by-
-//                       inverse of GPU LAPACKs);
+//                       inverse of GPU LAPACKs), fused with the next
+//                       column's update inside a super-panel (chol_diag
+//                       solves tile k + 1 itself);
 //       chol_update  -- trailing tiles (I, J), k < J <= I:
 //                       A_IJ <- A_IJ - A_Ik A_Jk^T;
 //     the two products run on the FP64 tensor cores (mma.sync m8n8k4 f64,
@@ -92,7 +94,7 @@ __device__ __forceinline__ void tile_product(const double *sa, const double *sb,
 // fetch, 113-200 us.)
 constexpr int kDiagThreads = 256;
 constexpr int kDP = kT + 1;  // shared pitch (column accesses conflict-free)
-constexpr int kDiagSmem = (2 * kT * kDP + 3 * 256 + kT) * (int)sizeof(double);
+constexpr int kDiagSmem = (2 * kT * kDP + 3 * 256 + kT + kT * kPitch) * (int)sizeof(double);
 
 // sqrt(d) and 1/sqrt(d) for d > 0 without the library's out-of-line slow paths
 // (their calls made the unrolled factor loop save its row registers to the
@@ -172,13 +174,17 @@ __device__ __forceinline__ void trailing16(double (*s)[kDP], int p0, int r0, int
         for (int bj = 0; bj <= bi; ++bj) s[r0 + 16 * bi + rr][r0 + 16 * bj + cc] -= acc[bi][bj];
 }
 
+// With solve_next, the kernel also solves the panel tile just below
+// (L_{k+1,k} = A_{k+1,k} L_kk^-T, the one the next diagonal tile's update
+// needs), so the panel kernel of this step only reads it.
 __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, int k, int *info,
-                                                          double *linv) {
+                                                          double *linv, int solve_next) {
     extern __shared__ double dsm[];
     double(*s)[kDP] = (double(*)[kDP])dsm;                // tile -> L
     double(*x)[kDP] = (double(*)[kDP])(dsm + kT * kDP);   // X = L^-1
     double *tmp = dsm + 2 * kT * kDP;                     // stage products, 3 x 16 x 16
     double *rinv = tmp + 3 * 256;  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
+    double *sn = rinv + kT;        // A_{k+1,k} (solve_next), pitch kPitch
     __shared__ int bad;
     const int b = blockIdx.y;
     if (info[b]) return;
@@ -186,21 +192,24 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
     const int64_t o = (int64_t)k * kT;
     const int m = (int)(n - o < kT ? n - o : kT);
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int m2 = solve_next ? (int)(n - o - kT < kT ? n - o - kT : kT) : 0;  // rows of tile k+1
     // rows/columns past the block factor as the identity; X starts as 0.
     // Every load in flight before the first shared store.
     {
         constexpr int kPer = kT * kT / kDiagThreads;
-        double v[kPer];
+        double v[kPer], vn[kPer];
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int e = t + q * kDiagThreads, rr = e >> 6, c = e & 63;
             v[q] = (rr < m && c < m) ? blk[(o + rr) * n + o + c] : (rr == c ? 1.0 : 0.0);
+            vn[q] = rr < m2 ? blk[(o + kT + rr) * n + o + c] : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int e = t + q * kDiagThreads, rr = e >> 6, c = e & 63;
             s[rr][c] = v[q];
             x[rr][c] = 0.0;
+            sn[rr * kPitch + c] = vn[q];
         }
     }
     if (t == 0) bad = 0;
@@ -280,53 +289,144 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
     }
     double *li = linv + (int64_t)b * kT * kT;
     for (int e = t; e < kT * kT; e += kDiagThreads) li[e] = x[e >> 6][e & 63];
+    if (m2 > 0) {
+        // L_{k+1,k} = A_{k+1,k} X^T on the DMMA pipe: warp w owns rows
+        // 16 (w / 2) .. + 15, columns 32 (w % 2) .. + 31
+        const int wr = (w >> 1) * 16, wc = (w & 1) * 32, fr = lane >> 2, fk = lane & 3;
+        double acc[2][4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+        for (int k0 = 0; k0 < kT; k0 += 4) {
+            double fa[2], fb[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) fa[i] = sn[(wr + 8 * i + fr) * kPitch + k0 + fk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) fb[j] = x[wc + 8 * j + fr][k0 + fk];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int rr = wr + 8 * i + fr;
+            if (rr >= m2) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double *p = blk + (o + kT + rr) * n + o + wc + 8 * j + 2 * fk;
+                p[0] = acc[i][j][0];
+                p[1] = acc[i][j][1];
+            }
+        }
+    }
 }
 
-// Panel: A_Ik <- A_Ik L_kk^-T for the tiles I > k below the diagonal.
-__global__ void __launch_bounds__(kGemmThreads) chol_trsm(double *a, int64_t n, int k,
-                                                          const int *info, const double *linv) {
+// Panel step k for the tiles below the diagonal.  CTA I (I >= k + 2) solves
+// L_Ik = A_Ik L_kk^-T (a 64 x 64 x 64 DMMA product with the inverse, the
+// TRSM-by-inverse of GPU LAPACKs) and stores it; with UPD (the next column
+// lies in the same super-panel) it then applies that column's update
+// A_{I,k+1} -= L_Ik L_{k+1,k}^T from the tile still in shared memory, and
+// CTA I = k + 1 applies the diagonal tile's A_{k+1,k+1} -= L_{k+1,k}
+// L_{k+1,k}^T (chol_diag already solved L_{k+1,k}).  One launch per step
+// instead of a solve and an update.
+constexpr int kPanelSmem = 3 * kT * kPitch * (int)sizeof(double);
+
+template <bool UPD>
+__global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n, int k,
+                                                           const int *info, const double *linv) {
     extern __shared__ double sm[];
-    double *sa = sm, *sb = sm + kT * kPitch;
+    double *sa = sm, *sx = sm + kT * kPitch, *sb = sm + 2 * kT * kPitch;
     const int b = blockIdx.y;
     if (info[b]) return;
     double *blk = a + (int64_t)b * n * n;
-    const int64_t I = (int64_t)k + 1 + blockIdx.x;
-    const int64_t r0 = I * kT, c0 = (int64_t)k * kT;
+    const int64_t I = (int64_t)k + (UPD ? 1 : 2) + blockIdx.x;
+    const bool own = UPD && I == k + 1;  // uniform per CTA
+    const int64_t r0 = I * kT, c0 = (int64_t)k * kT, c1 = c0 + kT;
     const int rows = (int)(n - r0 < kT ? n - r0 : kT);
+    const int rows1 = UPD ? (int)(n - c1 < kT ? n - c1 : kT) : 0;  // tile k + 1
     const double *li = linv + (int64_t)b * kT * kT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
     {
-        // every load of both tiles in flight before the first shared store
-        // (the loop form waited on one global round trip per few elements)
+        // every load in flight before the first shared store
         constexpr int kPer = kT * kT / kGemmThreads;
-        double va[kPer], vb[kPer];
+        double va[kPer], vx[kPer], vb[kPer];
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int e = threadIdx.x + q * kGemmThreads, rr = e >> 6, c = e & 63;
-            va[q] = rr < rows ? blk[(r0 + rr) * n + c0 + c] : 0.0;
-            vb[q] = li[e];
+            if (!own) {
+                va[q] = rr < rows ? blk[(r0 + rr) * n + c0 + c] : 0.0;
+                vx[q] = li[e];
+            }
+            if (UPD) vb[q] = rr < rows1 ? blk[(c1 + rr) * n + c0 + c] : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int e = threadIdx.x + q * kGemmThreads, rr = e >> 6, c = e & 63;
-            sa[rr * kPitch + c] = va[q];
-            sb[rr * kPitch + c] = vb[q];
+            if (!own) {
+                sa[rr * kPitch + c] = va[q];
+                sx[rr * kPitch + c] = vx[q];
+            }
+            if (UPD) sb[rr * kPitch + c] = vb[q];
         }
     }
     __syncthreads();
     double acc[4][4][2];
-    tile_product(sa, sb, acc);  // A_Ik Linv^T: B[q][c] = Linv[c][q]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+    if (!own) {
+        tile_product(sa, sx, acc);  // A_Ik Linv^T: B[q][c] = Linv[c][q]
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int rr = wr + 8 * i + (lane >> 2);
+            if (rr >= rows) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double *p = blk + (r0 + rr) * n + c0 + wc + 8 * j + 2 * (lane & 3);
+                p[0] = acc[i][j][0];
+                p[1] = acc[i][j][1];
+            }
+        }
+    }
+    if (!UPD) return;
+    double *sl = sb;
+    if (!own) {
+        __syncthreads();  // every warp is done reading sa
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double *q = sa + (wr + 8 * i + (lane >> 2)) * kPitch + wc + 8 * j + 2 * (lane & 3);
+                q[0] = acc[i][j][0];
+                q[1] = acc[i][j][1];
+            }
+        sl = sa;
+        __syncthreads();
+    }
+    tile_product(sl, sb, acc);  // L_Ik L_{k+1,k}^T
+    // C -= acc: every load first, then the stores
+    double cv[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int rr = wr + 8 * i + (lane >> 2);
-        if (rr >= rows) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int cc = wc + 8 * j + 2 * (lane & 3);
-            double *p = blk + (r0 + rr) * n + c0 + cc;
-            p[0] = acc[i][j][0];
-            p[1] = acc[i][j][1];
+            const double *p = blk + (r0 + rr) * n + c1 + cc;
+            cv[i][j][0] = (rr < rows && cc < rows1) ? p[0] : 0.0;
+            cv[i][j][1] = (rr < rows && cc + 1 < rows1) ? p[1] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = wr + 8 * i + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cc = wc + 8 * j + 2 * (lane & 3);
+            double *p = blk + (r0 + rr) * n + c1 + cc;
+            if (rr < rows && cc < rows1) p[0] = cv[i][j][0] - acc[i][j][0];
+            if (rr < rows && cc + 1 < rows1) p[1] = cv[i][j][1] - acc[i][j][1];
         }
     }
 }
@@ -635,9 +735,12 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch setup: %s", cudaGetErrorString(e));
     // dynamic shared-memory limits, raised once per device
     static std::atomic<uint64_t> done{0};
-    const int smem = 2 * kT * kPitch * (int)sizeof(double);
     if (!(done.load() & (1ull << (dev & 63)))) {
-        e = cudaFuncSetAttribute(chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaFuncSetAttribute(chol_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPanelSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_panel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(chol_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kUpdSmem);
@@ -711,26 +814,30 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         // column's own update touches the tiles it updated)
         bool pending_r = false;
         for (int k = p0; k < p1; ++k) {
-            chol_diag<<<dim3(1, (unsigned)batch), kDiagThreads, kDiagSmem, st>>>(d_lmat, n, k, info,
-                                                                            linv);
-            if (k + 1 < nt)
-                chol_trsm<<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads, smem, st>>>(
-                    d_lmat, n, k, info, linv);
+            chol_diag<<<dim3(1, (unsigned)batch), kDiagThreads, kDiagSmem, st>>>(
+                d_lmat, n, k, info, linv, k + 1 < nt);
+            if (k + 1 >= nt) continue;
             if (k + 1 < p1) {
-                if (split && k + 2 < p1) {
-                    cudaEventRecord(la.ev_h, st);  // panel k solved
-                    cudaStreamWaitEvent(la.sr, la.ev_h, 0);
-                }
+                // the next column's update also writes tiles the previous
+                // step's panel-local update wrote
                 if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);
-                if (split && k + 2 < p1) {
-                    update(st, k, k + 1, k + 1, k + 2, cap_all);       // column k+1: the chain
-                    update(la.sr, k, k + 1, k + 2, p1, cap_all);       // the rest, beside it
-                    cudaEventRecord(la.ev_r, la.sr);
-                    pending_r = true;
-                } else {
-                    update(st, k, k + 1, k + 1, p1, cap_all);
-                    pending_r = false;
+                chol_panel<true><<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads,
+                                   kPanelSmem, st>>>(d_lmat, n, k, info, linv);
+                pending_r = false;
+                if (k + 2 < p1) {  // the super-panel's later columns
+                    if (split) {
+                        cudaEventRecord(la.ev_h, st);  // panel k solved
+                        cudaStreamWaitEvent(la.sr, la.ev_h, 0);
+                        update(la.sr, k, k + 1, k + 2, p1, cap_all);
+                        cudaEventRecord(la.ev_r, la.sr);
+                        pending_r = true;
+                    } else {
+                        update(st, k, k + 1, k + 2, p1, cap_all);
+                    }
                 }
+            } else if (k + 2 < nt) {
+                chol_panel<false><<<dim3((unsigned)(nt - k - 2), (unsigned)batch), kGemmThreads,
+                                    kPanelSmem, st>>>(d_lmat, n, k, info, linv);
             }
         }
         if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);

@@ -199,6 +199,27 @@ def test_chol_batch_tiles_odd_and_ragged_sizes(n, nb):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("panel,split", [(1, 1), (2, 1), (3, 0), (8, 0), (32, 1)])
+def test_chol_batch_schedules_agree(monkeypatch, panel, split):
+    """Every super-panel width / stream split of the look-ahead schedule
+    (SFB_CHOL_PANEL, SFB_CHOL_SPLIT) factors to the oracle's L and D: the
+    fused panel kernel in both modes, the delayed and panel-local updates."""
+    monkeypatch.setenv("SFB_CHOL_PANEL", str(panel))
+    monkeypatch.setenv("SFB_CHOL_SPLIT", str(split))
+    n, nb = 700, 2
+    rng = np.random.default_rng(panel * 10 + split)
+    blocks = []
+    for _ in range(nb):
+        a = rng.standard_normal((n, n))
+        blocks.append(a @ a.T + n * np.eye(n))
+    data = np.vstack(blocks)
+    lmat, diag = sf.chol_batch(BatchedMatrix(data, nb))
+    rl, rd = og.chol_batch(data, nb)
+    assert np.allclose(lmat.data, rl, rtol=1e-10, atol=1e-12)
+    assert np.allclose(diag.data, rd, rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.gpu
 def test_not_positive_definite_pivot_in_a_later_tile():
     """The first failing minor lies past the first 64-tile (LAPACK info = its
     order); the other blocks of the batch are unaffected by the failure."""

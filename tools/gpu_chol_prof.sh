@@ -2,7 +2,7 @@
 # Cholesky timing at several super-panel widths + launch breakdown (one gpurun call)
 cd "${GRAFT_REPO_ROOT:-.}"
 for W in ${WS:-4 8 16 32}; do echo W=$W; SFB_CHOL_PANEL=$W python tools/chol_ab.py 2>&1 | head -1; done
-SFB_CHOL_PANEL=${WP:-8} ncu --metrics gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_dmma.avg.pct_of_peak_sustained_active --clock-control none -k regex:"chol|lower_mul" --csv python tools/chol_ab.py > gpurun_out/chol_launch.csv 2>&1
+SFB_CHOL_PANEL=${WP:-8} ncu --metrics gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active --clock-control none -k regex:"chol|lower_mul" --csv python tools/chol_ab.py > gpurun_out/chol_launch.csv 2>&1
 python3 - <<'PY'
 import csv, collections
 rows=[r for r in csv.reader(open('gpurun_out/chol_launch.csv')) if len(r)>10 and r[0].isdigit()]

@@ -38,14 +38,26 @@ def lines(rep):
     return res
 
 
+def merged(res):
+    # a report holding several launches lists every source line once per
+    # launch: sum them
+    acc = {}
+    for ie, te, ss, f, ln, src in res:
+        a = acc.setdefault((f, ln), [0, 0, 0, src])
+        a[0] += ie
+        a[1] += te
+        a[2] += ss
+    return [(a[0], a[1], a[2], f, ln, a[3]) for (f, ln), a in acc.items()]
+
+
 def main():
-    res = lines(sys.argv[1])
+    res = merged(lines(sys.argv[1]))
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
     ti = sum(r[0] for r in res) or 1
     tt = sum(r[1] for r in res) or 1
     ts = sum(r[2] for r in res) or 1
     print(f"warp inst {ti}, thread inst {tt} (avg active {tt / ti:.1f}), stall samples {ts}")
-    for ie, te, ss, f, ln, src in sorted(res, reverse=True)[:top]:
+    for ie, te, ss, f, ln, src in sorted(res, key=lambda r: -r[2])[:top]:
         print(f"{100 * ie / ti:5.1f}% inst {100 * ss / ts:5.1f}% stall act {te / max(ie, 1):4.1f}  "
               f"{f}:{ln}  {src}")
 
