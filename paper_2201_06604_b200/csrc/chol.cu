@@ -440,8 +440,9 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
 // loads synchronously.
 constexpr int kSlice = 32;
 constexpr int kSPitch = kSlice + 4;  // conflict-free fragment loads
-constexpr int kStages = 2;  // cp.async pipeline depth (3: 110 KB per CTA, slower -- the chain kernels no longer fit beside the bulk update)
-constexpr int kUpdSmem = kStages * 2 * kT * kSPitch * (int)sizeof(double);
+// cp.async pipeline depth: 2 (74 KB per CTA); 3 (110 KB) for the bulk update
+// via SFB_CHOL_STAGES (measured slower: two CTAs per SM instead of three)
+constexpr int upd_smem(int stages) { return stages * 2 * kT * kSPitch * (int)sizeof(double); }
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, int src_bytes) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
@@ -474,7 +475,7 @@ __device__ __forceinline__ void load_slice(double *sa, const double *blk, int64_
 // Persistent: CTAs stride over the linear index of (batch, J, I) tiles, so a
 // launch can be held to a fixed number of CTAs per SM (the bulk update leaves
 // room for the serial chain's kernels next to it).
-template <bool VEC>
+template <bool VEC, int kStages>
 __global__ void __launch_bounds__(kGemmThreads) chol_update(double *a, int64_t n, int nt, int k_lo,
                                                             int k_hi, int j_lo, int j_hi,
                                                             int batch, const int *info) {
@@ -742,11 +743,17 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
             e = cudaFuncSetAttribute(chol_panel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(chol_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kUpdSmem);
+            e = cudaFuncSetAttribute(chol_update<true, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, upd_smem(2));
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(chol_update<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem);
+            e = cudaFuncSetAttribute(chol_update<false, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, upd_smem(2));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_update<true, 3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, upd_smem(3));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(chol_update<false, 3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, upd_smem(3));
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kDiagSmem);
@@ -759,21 +766,29 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     // 64-column step factors its diagonal tile, solves its whole column below
     // and updates only the super-panel's later columns; the rest of the
     // trailing matrix gets one delayed update with K = the super-panel
-    const int W = std::max(1, tune_knob("SFB_CHOL_PANEL", 8));
+    const int W = std::max(1, tune_knob("SFB_CHOL_PANEL", 12));
     const bool vec = (n % 2) == 0;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int bulk_per_sm = std::max(1, tune_knob("SFB_CHOL_BULK_CTAS", 2));
+    const int bulk_per_sm = std::max(1, tune_knob("SFB_CHOL_BULK_CTAS", 3));
     // cap: CTAs per launch (the bulk update: bulk_per_sm per SM)
+    const int bulk_stages = tune_knob("SFB_CHOL_STAGES", 2) == 3 ? 3 : 2;
     auto update = [&](cudaStream_t us, int k_lo, int k_hi, int j_lo, int j_hi, int cap) {
         const int64_t tiles = (int64_t)(nt - j_lo) * (j_hi - j_lo) * batch;
         const unsigned grid = (unsigned)std::min<int64_t>(tiles, cap);
-        if (vec)
-            chol_update<true><<<grid, kGemmThreads, kUpdSmem, us>>>(d_lmat, n, nt, k_lo, k_hi,
-                                                                   j_lo, j_hi, (int)batch, info);
+        const bool deep = cap < (1 << 30) && bulk_stages == 3;
+        if (vec && deep)
+            chol_update<true, 3><<<grid, kGemmThreads, upd_smem(3), us>>>(
+                d_lmat, n, nt, k_lo, k_hi, j_lo, j_hi, (int)batch, info);
+        else if (vec)
+            chol_update<true, 2><<<grid, kGemmThreads, upd_smem(2), us>>>(
+                d_lmat, n, nt, k_lo, k_hi, j_lo, j_hi, (int)batch, info);
+        else if (deep)
+            chol_update<false, 3><<<grid, kGemmThreads, upd_smem(3), us>>>(
+                d_lmat, n, nt, k_lo, k_hi, j_lo, j_hi, (int)batch, info);
         else
-            chol_update<false><<<grid, kGemmThreads, kUpdSmem, us>>>(d_lmat, n, nt, k_lo, k_hi,
-                                                                    j_lo, j_hi, (int)batch, info);
+            chol_update<false, 2><<<grid, kGemmThreads, upd_smem(2), us>>>(
+                d_lmat, n, nt, k_lo, k_hi, j_lo, j_hi, (int)batch, info);
     };
     const int cap_all = 1 << 30, cap_bulk = nsm * bulk_per_sm;
     const bool split = tune_knob("SFB_CHOL_SPLIT", 1) != 0;
@@ -824,13 +839,25 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                 chol_panel<true><<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads,
                                    kPanelSmem, st>>>(d_lmat, n, k, info, linv);
                 pending_r = false;
-                if (k + 2 < p1) {  // the super-panel's later columns
+                if (k + 2 < p1) {
+                    // column k + 2 gets the contributions of columns p0 .. k
+                    // in one update (K = k + 1 - p0 tiles) beside the next
+                    // diagonal tile; column k + 1's own comes with the next
+                    // panel launch.  (Updating all later columns of the
+                    // super-panel by column k alone, K = one tile per
+                    // launch, ran the small updates at ~35 % DMMA.)
+                    const int lazy = tune_knob("SFB_CHOL_LAZY", 1);
                     if (split) {
                         cudaEventRecord(la.ev_h, st);  // panel k solved
                         cudaStreamWaitEvent(la.sr, la.ev_h, 0);
-                        update(la.sr, k, k + 1, k + 2, p1, cap_all);
+                        if (lazy)
+                            update(la.sr, p0, k + 1, k + 2, k + 3, cap_all);
+                        else
+                            update(la.sr, k, k + 1, k + 2, p1, cap_all);
                         cudaEventRecord(la.ev_r, la.sr);
                         pending_r = true;
+                    } else if (lazy) {
+                        update(st, p0, k + 1, k + 2, k + 3, cap_all);
                     } else {
                         update(st, k, k + 1, k + 2, p1, cap_all);
                     }
