@@ -32,6 +32,7 @@
 // summation order differs), which is how the reference's own tests compare.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
 
 #include <algorithm>
 #include <atomic>
@@ -92,15 +93,21 @@ __device__ __forceinline__ void tile_product(const double *sa, const double *sb,
 // three barriers per column measured 50-60 us per tile under ncu;
 // register-resident fully unrolled 64-column forms stalled on instruction
 // fetch, 113-200 us.)
+#ifdef DIAG_CLOCKS  // phase timing of chol_diag (experiment builds: -DDIAG_CLOCKS)
+#define DCLK(i) do { if (threadIdx.x == 0) dclk[i] = clock64(); } while (0)
+#else
+#define DCLK(i) do { } while (0)
+#endif
 constexpr int kDiagThreads = 256;
 constexpr int kDP = kT + 1;  // shared pitch (column accesses conflict-free)
-constexpr int kDiagSmem = (2 * kT * kDP + 3 * 256 + kT + kT * kPitch) * (int)sizeof(double);
+// s: 128 rows (the tile, then the tile below it), x: 64, stage products, 1/L_jj
+constexpr int kDiagSmem = (3 * kT * kDP + 3 * 256 + kT) * (int)sizeof(double);
 
 // sqrt(d) and 1/sqrt(d) for d > 0 without the library's out-of-line slow paths
 // (their calls made the unrolled factor loop save its row registers to the
-// stack): rsqrt.approx seed, two Newton steps, a residual-corrected root;
-// within a few ulp of LAPACK's sqrt and 1/sqrt (tolerance-level parity).
-// Subnormal-range d is scaled by 2^600 first (the seed flushes subnormals).
+// stack): rsqrt.approx seed and two Newton steps; within a few ulp of
+// LAPACK's sqrt and 1/sqrt (tolerance-level parity).  Subnormal-range d is
+// scaled by 2^600 first (the seed flushes subnormals).
 __device__ __forceinline__ void sqrt_rsqrt(double d, double &l, double &r) {
     const bool tiny = d < 0x1p-900;
     const double ds = tiny ? d * 0x1p600 : d;
@@ -109,23 +116,39 @@ __device__ __forceinline__ void sqrt_rsqrt(double d, double &l, double &r) {
     const double h = 0.5 * ds;
     y = y * fma(-h * y, y, 1.5);
     y = y * fma(-h * y, y, 1.5);
-    double x = ds * y;
-    x = fma(0.5 * y, fma(-x, x, ds), x);
-    l = tiny ? x * 0x1p-300 : x;
+    l = tiny ? ds * y * 0x1p-300 : ds * y;
     r = tiny ? y * 0x1p300 : y;
 }
 
-// (a): warp 0, lanes 0..15 own rows; returns 0 or the 1-based failing column
+// 1/d for d > 0: rcp.approx seed and one third-order correction (relative
+// error ~e^3, e <= 2^-20); subnormal-range d scaled as in sqrt_rsqrt
+__device__ __forceinline__ double recip(double d) {
+    const bool tiny = d < 0x1p-900;
+    const double ds = tiny ? d * 0x1p600 : d;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(ds));
+    const double e = fma(-ds, r, 1.0);
+    r = fma(r, fma(e, e, e), r);
+    return tiny ? r * 0x1p600 : r;
+}
+
+// (a): warp 0, lanes 0..15 own rows; returns 0 or the 1-based failing column.
+// The next pivot comes from the lane's own values: on lane j + 1,
+// dn = a_{j+1,j+1} - a_{j+1,j}^2 / d (= l_{j+1,j}^2), so the step-to-step
+// chain is one broadcast, a reciprocal and one fma (FP64 latency is what
+// bounds this loop); the roots and the shuffled column updates run beside it.
 __device__ __forceinline__ int factor16(double (*s)[kDP], double *rinv, int p0, int lane) {
     const int i = lane & 15;
     double v[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) v[c] = s[p0 + i][p0 + c];  // c > i: never read
     int fail = 0;  // no early exit: the loop stays unrolled (v in registers)
+    double dn = v[0];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        const double d = __shfl_sync(0xffffffffu, v[j], j);
+        const double d = __shfl_sync(0xffffffffu, dn, j);
         if (!(d > 0.0) && !fail) fail = j + 1;  // warp-uniform
+        if (j + 1 < 16) dn = fma(-(v[j] * v[j]), recip(d), v[j + 1]);
         double l, r;
         sqrt_rsqrt(d, l, r);
         const double sc = v[j] * r;
@@ -146,46 +169,69 @@ __device__ __forceinline__ int factor16(double (*s)[kDP], double *rinv, int p0, 
     return fail;
 }
 
-// (c): rows/columns [r0, 64) lower part -= A[:, p0:p0+16] A[:, p0:p0+16]^T,
+// (c): rows/columns [r0, 64) lower part, and with NEXT rows 64..127 (the tile
+// below) over columns [r0, 64), -= A[:, p0:p0+16] A[:, p0:p0+16]^T;
 // NB = (64 - r0) / 16 sub-blocks per side
-template <int NB>
+template <int NB, bool NEXT>
 __device__ __forceinline__ void trailing16(double (*s)[kDP], int p0, int r0, int t) {
+    constexpr int NR = NB + (NEXT ? 4 : 0);
     const int rr = t >> 4, cc = t & 15;
-    double acc[NB][NB];
+    auto row = [&](int bi) { return bi < NB ? r0 + 16 * bi + rr : kT + 16 * (bi - NB) + rr; };
+    double acc[NR][NB];
 #pragma unroll
-    for (int bi = 0; bi < NB; ++bi)
+    for (int bi = 0; bi < NR; ++bi)
 #pragma unroll
         for (int bj = 0; bj < NB; ++bj) acc[bi][bj] = 0.0;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-        double rv[NB], cv[NB];
+        double rv[NR], cv[NB];
 #pragma unroll
-        for (int bi = 0; bi < NB; ++bi) rv[bi] = s[r0 + 16 * bi + rr][p0 + c];
+        for (int bi = 0; bi < NR; ++bi) rv[bi] = s[row(bi)][p0 + c];
 #pragma unroll
         for (int bj = 0; bj < NB; ++bj) cv[bj] = s[r0 + 16 * bj + cc][p0 + c];
 #pragma unroll
-        for (int bi = 0; bi < NB; ++bi)
+        for (int bi = 0; bi < NR; ++bi)
 #pragma unroll
-            for (int bj = 0; bj <= bi; ++bj) acc[bi][bj] += rv[bi] * cv[bj];
+            for (int bj = 0; bj < NB; ++bj)
+                if (bi >= NB || bj <= bi) acc[bi][bj] += rv[bi] * cv[bj];
     }
 #pragma unroll
-    for (int bi = 0; bi < NB; ++bi)
+    for (int bi = 0; bi < NR; ++bi)
 #pragma unroll
-        for (int bj = 0; bj <= bi; ++bj) s[r0 + 16 * bi + rr][r0 + 16 * bj + cc] -= acc[bi][bj];
+        for (int bj = 0; bj < NB; ++bj)
+            if (bi >= NB || bj <= bi) s[row(bi)][r0 + 16 * bj + cc] -= acc[bi][bj];
 }
 
-// With solve_next, the kernel also solves the panel tile just below
-// (L_{k+1,k} = A_{k+1,k} L_kk^-T, the one the next diagonal tile's update
-// needs), so the panel kernel of this step only reads it.
+// Factor tile (k, k) of every block and store the inverse of its lower factor.
+// The tile's factorisation is on the critical path of every panel step, so it
+// is blocked in 16-column steps to keep the number of block-wide barriers
+// small (~20 instead of 3 per column):
+//   (a) warp 0 factors the 16 x 16 diagonal block in registers (lane i holds
+//       row i; the column is broadcast with shuffles, no barriers);
+//   (b) the rows below solve against it (one thread per row, forward
+//       substitution in registers);
+//   (c) the trailing lower part is updated (thread (rr, cc) of every 16 x 16
+//       sub-block, the sub-blocks' row/column values loaded once per column);
+// then the inverse X = L^-1: the four diagonal blocks by forward substitution
+// (warp p, lane c = column c of X_pp), the off-diagonal blocks in three stages
+// X_ip = -X_ii sum_{p <= m < i} L_im X_mp.  With solve_next the tile below,
+// (k + 1, k), rides along as 64 more panel rows in (b) and (c), so L_{k+1,k}
+// (which the next diagonal tile's update needs first) leaves with L_kk.
+// (Unblocked 64-step forms with three barriers per column measured 50-60 us
+// per tile under ncu; register-resident fully unrolled 64-column forms
+// stalled on instruction fetch, 113-200 us.)
 __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, int k, int *info,
                                                           double *linv, int solve_next) {
     extern __shared__ double dsm[];
-    double(*s)[kDP] = (double(*)[kDP])dsm;                // tile -> L
-    double(*x)[kDP] = (double(*)[kDP])(dsm + kT * kDP);   // X = L^-1
-    double *tmp = dsm + 2 * kT * kDP;                     // stage products, 3 x 16 x 16
+    double(*s)[kDP] = (double(*)[kDP])dsm;                    // tile + tile below -> L
+    double(*x)[kDP] = (double(*)[kDP])(dsm + 2 * kT * kDP);   // X = L^-1
+    double *tmp = dsm + 3 * kT * kDP;                         // stage products, 3 x 16 x 16
     double *rinv = tmp + 3 * 256;  // 1 / L[j][j] (LAPACK dpotf2 scales by the reciprocal too)
-    double *sn = rinv + kT;        // A_{k+1,k} (solve_next), pitch kPitch
     __shared__ int bad;
+#ifdef DIAG_CLOCKS
+    __shared__ long long dclk[24];
+#endif
+    DCLK(0);
     const int b = blockIdx.y;
     if (info[b]) return;
     double *blk = a + (int64_t)b * n * n;
@@ -193,6 +239,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
     const int m = (int)(n - o < kT ? n - o : kT);
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
     const int m2 = solve_next ? (int)(n - o - kT < kT ? n - o - kT : kT) : 0;  // rows of tile k+1
+    const bool next = m2 > 0;
     // rows/columns past the block factor as the identity; X starts as 0.
     // Every load in flight before the first shared store.
     {
@@ -208,12 +255,14 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
         for (int q = 0; q < kPer; ++q) {
             const int e = t + q * kDiagThreads, rr = e >> 6, c = e & 63;
             s[rr][c] = v[q];
+            s[kT + rr][c] = vn[q];
             x[rr][c] = 0.0;
-            sn[rr * kPitch + c] = vn[q];
         }
     }
     if (t == 0) bad = 0;
     __syncthreads();
+    DCLK(1);
+    const int rend = next ? 2 * kT : kT;  // panel rows end
     for (int p = 0; p < 4; ++p) {
         const int p0 = 16 * p, r0 = p0 + 16;
         if (w == 0) {
@@ -221,9 +270,9 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
             if (f && lane == 0) bad = p0 + f;
         }
         __syncthreads();
+        DCLK(2 + 3 * p);
         if (bad) break;
-        if (p == 3) break;
-        if (t < kT - r0) {  // (b) row r0 + t of the panel: Y L_pp^T = A
+        if (t < rend - r0) {  // (b) row r0 + t of the panel: Y L_pp^T = A
             const int r = r0 + t;
             double y[16];
 #pragma unroll
@@ -232,20 +281,36 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
             for (int c = 0; c < 16; ++c) {
                 y[c] *= rinv[p0 + c];
 #pragma unroll
-                for (int q = c + 1; q < 16; ++q) y[q] -= y[c] * s[p0 + q][p0 + c];
+                for (int q = 1; q < 16; ++q)
+                    if (q > c) y[q] -= y[c] * s[p0 + q][p0 + c];
             }
 #pragma unroll
             for (int c = 0; c < 16; ++c) s[r][p0 + c] = y[c];
         }
         __syncthreads();
-        if (p == 0) trailing16<3>(s, p0, r0, t);
-        else if (p == 1) trailing16<2>(s, p0, r0, t);
-        else trailing16<1>(s, p0, r0, t);
+        DCLK(3 + 3 * p);
+        if (p == 3) break;
+        if (next) {
+            if (p == 0) trailing16<3, true>(s, p0, r0, t);
+            else if (p == 1) trailing16<2, true>(s, p0, r0, t);
+            else trailing16<1, true>(s, p0, r0, t);
+        } else {
+            if (p == 0) trailing16<3, false>(s, p0, r0, t);
+            else if (p == 1) trailing16<2, false>(s, p0, r0, t);
+            else trailing16<1, false>(s, p0, r0, t);
+        }
         __syncthreads();
+        DCLK(4 + 3 * p);
     }
     if (bad) {
         if (t == 0) info[b] = (int)(o + bad);  // LAPACK info: order of the failing minor
         return;
+    }
+    // L_kk and L_{k+1,k} are final: stored while the inverse is formed
+    for (int e = t; e < kT * kT; e += kDiagThreads) {
+        const int rr = e >> 6, c = e & 63;
+        if (rr < m && c <= rr) blk[(o + rr) * n + o + c] = s[rr][c];
+        if (rr < m2) blk[(o + kT + rr) * n + o + c] = s[kT + rr][c];
     }
     // X_pp = L_pp^-1: warp p, lane c computes column c (L X = I, right-looking)
     if (w < 4 && lane < 16) {
@@ -257,71 +322,55 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
         for (int i = 0; i < 16; ++i) {
             xv[i] *= rinv[p0 + i];
 #pragma unroll
-            for (int q = i + 1; q < 16; ++q) xv[q] -= s[p0 + q][p0 + i] * xv[i];
+            for (int q = 1; q < 16; ++q)
+                if (q > i) xv[q] -= s[p0 + q][p0 + i] * xv[i];
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) x[p0 + i][p0 + c] = xv[i];
     }
     __syncthreads();
-    // X_ip = -X_ii sum_{p <= q < i} L_iq X_qp, by distance d = i - p
-    for (int d = 1; d < 4; ++d) {
-        const int nblk = 4 - d;
-        for (int e = t; e < nblk * 256; e += kDiagThreads) {
-            const int p = e >> 8, rr = (e >> 4) & 15, c = e & 15, i = p + d;
-            double acc = 0.0;
-#pragma unroll 16
-            for (int q = 16 * p; q < 16 * i; ++q) acc += s[16 * i + rr][q] * x[q][16 * p + c];
-            tmp[e] = acc;
-        }
-        __syncthreads();
-        for (int e = t; e < nblk * 256; e += kDiagThreads) {
-            const int p = e >> 8, rr = (e >> 4) & 15, c = e & 15, i = p + d;
-            double acc = 0.0;
+    DCLK(14);
+    // X_ip = -X_ii sum_{p <= q < i} L_iq X_qp, by distance d = i - p: the
+    // 16 x 16 block products on the DMMA pipe, one 8 x 8 output tile per warp
+    // (the scalar form was shared-load bound, ~9k cycles for the three stages)
+    {
+        const int fr = lane >> 2, fk = lane & 3;
+        for (int d = 1; d < 4; ++d) {
+            const int ntile = (4 - d) * 4;
+            for (int tl = w; tl < ntile; tl += kDiagThreads / 32) {
+                const int p = tl >> 2, i = p + d, tr = ((tl >> 1) & 1) * 8, tc = (tl & 1) * 8;
+                double c0 = 0.0, c1 = 0.0;
+                for (int q0 = 16 * p; q0 < 16 * i; q0 += 4)
+                    dmma(c0, c1, s[16 * i + tr + fr][q0 + fk], x[q0 + fk][16 * p + tc + fr]);
+                double *tp = tmp + p * 256 + (tr + fr) * 16 + tc + 2 * fk;
+                tp[0] = c0;
+                tp[1] = c1;
+            }
+            __syncthreads();
+            for (int tl = w; tl < ntile; tl += kDiagThreads / 32) {
+                const int p = tl >> 2, i = p + d, tr = ((tl >> 1) & 1) * 8, tc = (tl & 1) * 8;
+                double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) acc += x[16 * i + rr][16 * i + q] * tmp[p * 256 + q * 16 + c];
-            x[16 * i + rr][16 * p + c] = -acc;
+                for (int q0 = 0; q0 < 16; q0 += 4)
+                    dmma(c0, c1, x[16 * i + tr + fr][16 * i + q0 + fk],
+                         tmp[p * 256 + (q0 + fk) * 16 + tc + fr]);
+                x[16 * i + tr + fr][16 * p + tc + 2 * fk] = -c0;
+                x[16 * i + tr + fr][16 * p + tc + 2 * fk + 1] = -c1;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
-    for (int e = t; e < kT * kT; e += kDiagThreads) {
-        const int rr = e >> 6, c = e & 63;
-        if (rr < m && c <= rr) blk[(o + rr) * n + o + c] = s[rr][c];
-    }
+    DCLK(15);
     double *li = linv + (int64_t)b * kT * kT;
     for (int e = t; e < kT * kT; e += kDiagThreads) li[e] = x[e >> 6][e & 63];
-    if (m2 > 0) {
-        // L_{k+1,k} = A_{k+1,k} X^T on the DMMA pipe: warp w owns rows
-        // 16 (w / 2) .. + 15, columns 32 (w % 2) .. + 31
-        const int wr = (w >> 1) * 16, wc = (w & 1) * 32, fr = lane >> 2, fk = lane & 3;
-        double acc[2][4][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll 4
-        for (int k0 = 0; k0 < kT; k0 += 4) {
-            double fa[2], fb[4];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) fa[i] = sn[(wr + 8 * i + fr) * kPitch + k0 + fk];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) fb[j] = x[wc + 8 * j + fr][k0 + fk];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int rr = wr + 8 * i + fr;
-            if (rr >= m2) continue;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                double *p = blk + (o + kT + rr) * n + o + wc + 8 * j + 2 * fk;
-                p[0] = acc[i][j][0];
-                p[1] = acc[i][j][1];
-            }
-        }
+    DCLK(16);
+#ifdef DIAG_CLOCKS
+    if (t == 0 && b == 0 && k == 5) {
+        printf("diag k=5 cycles:");
+        for (int q = 1; q < 17; ++q) printf(" %lld", dclk[q] - dclk[q - 1]);
+        printf("\n");
     }
+#endif
 }
 
 // Panel step k for the tiles below the diagonal.  CTA I (I >= k + 2) solves
@@ -472,20 +521,30 @@ __device__ __forceinline__ void load_slice(double *sa, const double *blk, int64_
     }
 }
 
-// Persistent: CTAs stride over the linear index of (batch, J, I) tiles, so a
-// launch can be held to a fixed number of CTAs per SM (the bulk update leaves
-// room for the serial chain's kernels next to it).
+// CTAs stride over the linear index of the (batch, J, I >= J) tiles -- the
+// lower trapezoid, column by column, so neighbouring CTAs share A_Jk -- and a
+// launch can be held to a fixed number of CTAs per SM (SFB_CHOL_BULK_CTAS;
+// the default launches one CTA per tile).
+__device__ __forceinline__ int64_t trap_start(int64_t jj, int64_t R) {
+    return jj * R - jj * (jj - 1) / 2;  // tiles in columns before jj (R - c in column c)
+}
+
 template <bool VEC, int kStages>
 __global__ void __launch_bounds__(kGemmThreads) chol_update(double *a, int64_t n, int nt, int k_lo,
                                                             int k_hi, int j_lo, int j_hi,
                                                             int batch, const int *info) {
     extern __shared__ double sm[];
-    const int64_t R = nt - j_lo, per = R * (j_hi - j_lo);
+    const int64_t R = nt - j_lo, Wc = j_hi - j_lo, per = trap_start(Wc, R);
     for (int64_t x = blockIdx.x; x < per * batch; x += gridDim.x) {
         const int b = (int)(x / per);
         const int64_t y = x - b * per;
-        const int64_t I = j_lo + y % R, J = j_lo + y / R;
-        if (I < J || info[b]) continue;  // uniform per CTA
+        const double q = (double)(2 * R + 1);
+        int64_t jj = (int64_t)((q - sqrt(q * q - 8.0 * (double)y)) * 0.5);
+        jj = jj < 0 ? 0 : (jj >= Wc ? Wc - 1 : jj);
+        while (jj + 1 < Wc && trap_start(jj + 1, R) <= y) ++jj;
+        while (jj > 0 && trap_start(jj, R) > y) --jj;
+        const int64_t J = j_lo + jj, I = J + (y - trap_start(jj, R));
+        if (info[b]) continue;  // uniform per CTA
         double *blk = a + (int64_t)b * n * n;
         const int64_t ri = I * kT, rj = J * kT;
         const int rows = (int)(n - ri < kT ? n - ri : kT);
@@ -766,15 +825,16 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     // 64-column step factors its diagonal tile, solves its whole column below
     // and updates only the super-panel's later columns; the rest of the
     // trailing matrix gets one delayed update with K = the super-panel
-    const int W = std::max(1, tune_knob("SFB_CHOL_PANEL", 12));
+    const int W = std::max(1, tune_knob("SFB_CHOL_PANEL", 8));
     const bool vec = (n % 2) == 0;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int bulk_per_sm = std::max(1, tune_knob("SFB_CHOL_BULK_CTAS", 3));
+    const int bulk_per_sm = tune_knob("SFB_CHOL_BULK_CTAS", 0);  // 0: one CTA per tile
     // cap: CTAs per launch (the bulk update: bulk_per_sm per SM)
     const int bulk_stages = tune_knob("SFB_CHOL_STAGES", 2) == 3 ? 3 : 2;
     auto update = [&](cudaStream_t us, int k_lo, int k_hi, int j_lo, int j_hi, int cap) {
-        const int64_t tiles = (int64_t)(nt - j_lo) * (j_hi - j_lo) * batch;
+        const int64_t R = nt - j_lo, Wc = j_hi - j_lo;
+        const int64_t tiles = (Wc * R - Wc * (Wc - 1) / 2) * batch;  // I >= J only
         const unsigned grid = (unsigned)std::min<int64_t>(tiles, cap);
         const bool deep = cap < (1 << 30) && bulk_stages == 3;
         if (vec && deep)
@@ -790,7 +850,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
             chol_update<false, 2><<<grid, kGemmThreads, upd_smem(2), us>>>(
                 d_lmat, n, nt, k_lo, k_hi, j_lo, j_hi, (int)batch, info);
     };
-    const int cap_all = 1 << 30, cap_bulk = nsm * bulk_per_sm;
+    const int cap_all = 1 << 30, cap_bulk = bulk_per_sm > 0 ? nsm * bulk_per_sm : cap_all;
     const bool split = tune_knob("SFB_CHOL_SPLIT", 1) != 0;
     // Look-ahead: after super-panel i is factored, its update of the next
     // super-panel's columns (a_i) runs on the caller's stream, the bulk update
