@@ -388,6 +388,10 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
                                                            const int *info, const double *linv) {
     extern __shared__ double sm[];
     double *sa = sm, *sx = sm + kT * kPitch, *sb = sm + 2 * kT * kPitch;
+#ifdef DIAG_CLOCKS
+    __shared__ long long dclk[8];
+#endif
+    DCLK(0);
     const int b = blockIdx.y;
     if (info[b]) return;
     double *blk = a + (int64_t)b * n * n;
@@ -423,6 +427,7 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
         }
     }
     __syncthreads();
+    DCLK(1);
     double acc[4][4][2];
     if (!own) {
         tile_product(sa, sx, acc);  // A_Ik Linv^T: B[q][c] = Linv[c][q]
@@ -438,6 +443,7 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
             }
         }
     }
+    DCLK(2);
     if (!UPD) return;
     double *sl = sb;
     if (!own) {
@@ -453,7 +459,9 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
         sl = sa;
         __syncthreads();
     }
+    DCLK(3);
     tile_product(sl, sb, acc);  // L_Ik L_{k+1,k}^T
+    DCLK(4);
     // C -= acc: every load first, then the stores
     double cv[4][4][2];
 #pragma unroll
@@ -478,6 +486,14 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
             if (rr < rows && cc + 1 < rows1) p[1] = cv[i][j][1] - acc[i][j][1];
         }
     }
+#ifdef DIAG_CLOCKS
+    DCLK(5);
+    if (threadIdx.x == 0 && b == 0 && k == 5 && blockIdx.x == 1) {
+        printf("panel k=5 I=7 cycles:");
+        for (int q = 1; q < 6; ++q) printf(" %lld", dclk[q] - dclk[q - 1]);
+        printf("\n");
+    }
+#endif
 }
 
 // Update of the tiles (I, J), J in [j_lo, j_hi), I in [J, nt):
