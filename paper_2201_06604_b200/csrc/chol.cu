@@ -162,6 +162,7 @@ __device__ __forceinline__ int factor16(double (*s)[kDP], double *rinv, int p0, 
             }
         }
     }
+    __syncwarp();  // lanes 16..31 read the same rows (mirrors of lanes 0..15)
     if (lane < 16 && !fail) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) s[p0 + i][p0 + c] = v[c];  // c > i: unchanged values
