@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <atomic>
@@ -951,6 +952,9 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
             update(st, p0, p1, p1, p2, cap_all);  // a: the next super-panel's columns
             if (p2 < nt) {
                 cudaStreamWaitEvent(la.sb, la.ev_a, 0);
+#ifdef DIAG_CLOCKS  // experiment builds: time the schedule without the bulk update
+                if (!getenv("SFB_CHOL_NO_BULK"))
+#endif
                 update(la.sb, p0, p1, p2, nt, cap_bulk);  // b: the rest
                 cudaEventRecord(la.ev_b, la.sb);
                 pending_b = true;
