@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "sfb_internal.h"
 
@@ -781,7 +782,10 @@ struct LookAhead {
     std::mutex mu;
     cudaStream_t sb = nullptr, sh = nullptr;  // bulk update (low priority), chain (high)
     cudaStream_t sr = nullptr;                // super-panel-local updates beside the chain
+    cudaStream_t sc = nullptr;                // the next super-panel's later columns
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s = nullptr, ev_h = nullptr, ev_r = nullptr;
+    cudaEvent_t ev_x = nullptr;
+    std::vector<cudaEvent_t> ev_col;  // per column of the next super-panel (sc)
 };
 
 static LookAhead &look_ahead(int dev) {
@@ -892,8 +896,24 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&la.sr, cudaStreamNonBlocking, hi);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_h, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_r, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&la.sc, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_x, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch streams: %s", cudaGetErrorString(e));
     }
+    while (e == cudaSuccess && (int)la.ev_col.size() < W) {
+        cudaEvent_t ev = nullptr;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) la.ev_col.push_back(ev);
+    }
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch events: %s", cudaGetErrorString(e));
+    // Super-panel columns after the first get their update by the previous
+    // super-panel (its "a" part) one column per launch on stream sc, and the
+    // chain waits for each column just before it touches it: only the first
+    // column's part sits on the serial path (a schedule without the bulk
+    // update measured 6.5 of 9.1 ms, i.e. the chain and the whole "a" update
+    // were the critical path).
+    const bool split_a = split && tune_knob("SFB_CHOL_SPLIT_A", 1) != 0;
+    bool col_pending = false;  // this super-panel's columns > p0 have sc events
     const cudaStream_t caller = st;
     cudaEventRecord(la.ev_s, caller);  // the copy into d_lmat, the info reset, linv
     cudaStreamWaitEvent(la.sh, la.ev_s, 0);
@@ -912,8 +932,10 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
             if (k + 1 >= nt) continue;
             if (k + 1 < p1) {
                 // the next column's update also writes tiles the previous
-                // step's panel-local update wrote
+                // step's panel-local update (and the previous super-panel's
+                // column update on sc) wrote
                 if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);
+                if (col_pending) cudaStreamWaitEvent(st, la.ev_col[k + 1 - p0], 0);
                 chol_panel<true><<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads,
                                    kPanelSmem, st>>>(d_lmat, n, k, info, linv);
                 pending_r = false;
@@ -928,6 +950,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                     if (split) {
                         cudaEventRecord(la.ev_h, st);  // panel k solved
                         cudaStreamWaitEvent(la.sr, la.ev_h, 0);
+                        if (col_pending) cudaStreamWaitEvent(la.sr, la.ev_col[k + 2 - p0], 0);
                         if (lazy)
                             update(la.sr, p0, k + 1, k + 2, k + 3, cap_all);
                         else
@@ -935,6 +958,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                         cudaEventRecord(la.ev_r, la.sr);
                         pending_r = true;
                     } else if (lazy) {
+                        if (col_pending) cudaStreamWaitEvent(st, la.ev_col[k + 2 - p0], 0);
                         update(st, p0, k + 1, k + 2, k + 3, cap_all);
                     } else {
                         update(st, k, k + 1, k + 2, p1, cap_all);
@@ -949,7 +973,21 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         if (p1 < nt) {
             cudaEventRecord(la.ev_a, st);  // super-panel p0 factored
             if (pending_b) cudaStreamWaitEvent(st, la.ev_b, 0);  // b of the previous super-panel
-            update(st, p0, p1, p1, p2, cap_all);  // a: the next super-panel's columns
+            if (split_a && p2 - p1 > 1) {
+                // a: the next super-panel's first column on the chain, the
+                // others one launch each on sc
+                cudaEventRecord(la.ev_x, st);
+                cudaStreamWaitEvent(la.sc, la.ev_x, 0);
+                update(st, p0, p1, p1, p1 + 1, cap_all);
+                for (int c = p1 + 1; c < p2; ++c) {
+                    update(la.sc, p0, p1, c, c + 1, cap_all);
+                    cudaEventRecord(la.ev_col[c - p1], la.sc);
+                }
+                col_pending = true;
+            } else {
+                update(st, p0, p1, p1, p2, cap_all);  // a: the next super-panel's columns
+                col_pending = false;
+            }
             if (p2 < nt) {
                 cudaStreamWaitEvent(la.sb, la.ev_a, 0);
 #ifdef DIAG_CLOCKS  // experiment builds: time the schedule without the bulk update
