@@ -784,7 +784,7 @@ struct LookAhead {
     cudaStream_t sr = nullptr;                // super-panel-local updates beside the chain
     cudaStream_t sc = nullptr;                // the next super-panel's later columns
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s = nullptr, ev_h = nullptr, ev_r = nullptr;
-    cudaEvent_t ev_x = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_be = nullptr;
     std::vector<cudaEvent_t> ev_col;  // per column of the next super-panel (sc)
 };
 
@@ -898,6 +898,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_r, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&la.sc, cudaStreamNonBlocking, hi);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_x, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&la.ev_be, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(SFB_E_CUDA, "chol_batch streams: %s", cudaGetErrorString(e));
     }
     while (e == cudaSuccess && (int)la.ev_col.size() < W) {
@@ -914,6 +915,10 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     // were the critical path).
     const bool split_a = split && tune_knob("SFB_CHOL_SPLIT_A", 1) != 0;
     bool col_pending = false;  // this super-panel's columns > p0 have sc events
+    // The bulk update of super-panel i is split: the columns of super-panel
+    // i + 2 first (what the next "a" update waits for), then the rest, which
+    // keeps running beside super-panel i + 1's chain.
+    const bool split_b = tune_knob("SFB_CHOL_SPLIT_B", 1) != 0;
     const cudaStream_t caller = st;
     cudaEventRecord(la.ev_s, caller);  // the copy into d_lmat, the info reset, linv
     cudaStreamWaitEvent(la.sh, la.ev_s, 0);
@@ -993,8 +998,18 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
 #ifdef DIAG_CLOCKS  // experiment builds: time the schedule without the bulk update
                 if (!getenv("SFB_CHOL_NO_BULK"))
 #endif
-                update(la.sb, p0, p1, p2, nt, cap_bulk);  // b: the rest
-                cudaEventRecord(la.ev_b, la.sb);
+                {
+                    const int p3 = std::min(p2 + W, nt);
+                    if (split_b && p3 < nt) {
+                        update(la.sb, p0, p1, p2, p3, cap_bulk);  // b, near columns
+                        cudaEventRecord(la.ev_b, la.sb);
+                        update(la.sb, p0, p1, p3, nt, cap_bulk);  // b, the rest
+                    } else {
+                        update(la.sb, p0, p1, p2, nt, cap_bulk);  // b: the rest
+                        cudaEventRecord(la.ev_b, la.sb);
+                    }
+                }
+                cudaEventRecord(la.ev_be, la.sb);
                 pending_b = true;
             } else {
                 pending_b = false;
@@ -1002,7 +1017,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         }
         e = cudaGetLastError();
     }
-    if (pending_b) cudaStreamWaitEvent(st, la.ev_b, 0);
+    if (pending_b) cudaStreamWaitEvent(st, la.ev_be, 0);  // every bulk update
     cudaEventRecord(la.ev_s, st);
     cudaStreamWaitEvent(caller, la.ev_s, 0);
     st = caller;
