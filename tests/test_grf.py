@@ -220,6 +220,43 @@ def test_chol_batch_schedules_agree(monkeypatch, panel, split):
 
 
 @pytest.mark.gpu
+def test_chol_batch_concurrent_threads_and_streams():
+    """Two host threads factor different batches on their own CUDA streams at
+    once (the per-device look-ahead streams, events and scratch are shared
+    under a lock): each result equals the same call made alone."""
+    import threading
+
+    import torch
+
+    rng = np.random.default_rng(21)
+    mats = []
+    for n in (300, 515):
+        a = rng.standard_normal((2 * n, n))
+        blocks = [a[:n] @ a[:n].T + n * np.eye(n), a[n:] @ a[n:].T + n * np.eye(n)]
+        mats.append(BatchedMatrix(np.vstack(blocks), 2))
+    alone = [sf.chol_batch(m) for m in mats]
+    alone = [(lm.data.copy(), dg.data.copy()) for lm, dg in alone]
+    out = [None, None]
+
+    def work(q):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                lm, dg = sf.chol_batch(mats[q])
+            s.synchronize()
+            out[q] = (lm.data, dg.data)
+
+    ts = [threading.Thread(target=work, args=(q,)) for q in (0, 1)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for q in (0, 1):
+        assert np.array_equal(out[q][0], alone[q][0])
+        assert np.array_equal(out[q][1], alone[q][1])
+
+
+@pytest.mark.gpu
 def test_not_positive_definite_pivot_in_a_later_tile():
     """The first failing minor lies past the first 64-tile (LAPACK info = its
     order); the other blocks of the batch are unaffected by the failure."""
