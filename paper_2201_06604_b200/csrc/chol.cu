@@ -140,34 +140,41 @@ __device__ __forceinline__ double recip(double d) {
 // chain is one broadcast, a reciprocal and one fma (FP64 latency is what
 // bounds this loop); the roots and the shuffled column updates run beside it.
 __device__ __forceinline__ int factor16(double (*s)[kDP], double *rinv, int p0, int lane) {
-    const int i = lane & 15;
-    double v[16];
+    // lane = 16 h + i holds row i, columns c = 2 cl + h (cl < 8): both halves
+    // of the warp carry distinct columns, so a step's column broadcast and
+    // update is ~(16 - j) / 2 shuffles and fmas per lane instead of 15 - j
+    const int i = lane & 15, h = lane >> 4;
+    double v[8];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) v[c] = s[p0 + i][p0 + c];  // c > i: never read
+    for (int cl = 0; cl < 8; ++cl) v[cl] = s[p0 + i][p0 + 2 * cl + h];  // c > i: never read
     int fail = 0;  // no early exit: the loop stays unrolled (v in registers)
-    double dn = v[0];
+    double dn = v[0];  // pivot 0 on lane 0 (row 0, column 0)
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        const double d = __shfl_sync(0xffffffffu, dn, j);
+        const int hj = j & 1, jl = j >> 1;  // owner half / local index of column j
+        const double raw = __shfl_sync(0xffffffffu, v[jl], hj * 16 + i);  // a_ij (unscaled)
+        const double d = __shfl_sync(0xffffffffu, dn, hj * 16 + j);
         if (!(d > 0.0) && !fail) fail = j + 1;  // warp-uniform
-        if (j + 1 < 16) dn = fma(-(v[j] * v[j]), recip(d), v[j + 1]);
+        // next pivot on lane (j+1 & 1) 16 + j + 1: a_{j+1,j+1} - a_{j+1,j}^2 / d
+        if (j + 1 < 16) dn = fma(-(raw * raw), recip(d), v[(j + 1) >> 1]);
         double l, r;
         sqrt_rsqrt(d, l, r);
-        const double sc = v[j] * r;
-        v[j] = i == j ? l : (i > j ? sc : v[j]);
-        if (lane == j) rinv[p0 + j] = r;
+        const double lij = raw * r;
+        if (lane == hj * 16 + j) rinv[p0 + j] = r;
 #pragma unroll
-        for (int c = 1; c < 16; ++c) {  // constant trip count: unrolled before the j loop
-            if (c > j) {
-                const double lc = __shfl_sync(0xffffffffu, v[j], c);
-                if (i >= c) v[c] -= v[j] * lc;
+        for (int cl = 0; cl < 8; ++cl) {
+            if (2 * cl + 1 > j) {  // some column 2 cl + h lies right of j
+                const int c = 2 * cl + h;
+                const double lc = __shfl_sync(0xffffffffu, v[jl], hj * 16 + c) * r;
+                if (c > j && i >= c) v[cl] -= lij * lc;
             }
         }
+        // column j itself, on its owner half (after the shuffles above read it)
+        v[jl] = h != hj ? v[jl] : (i == j ? l : (i > j ? lij : v[jl]));
     }
-    __syncwarp();  // lanes 16..31 read the same rows (mirrors of lanes 0..15)
-    if (lane < 16 && !fail) {
+    if (!fail) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) s[p0 + i][p0 + c] = v[c];  // c > i: unchanged values
+        for (int cl = 0; cl < 8; ++cl) s[p0 + i][p0 + 2 * cl + h] = v[cl];  // c > i: unchanged
     }
     return fail;
 }
