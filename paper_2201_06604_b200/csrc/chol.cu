@@ -7,21 +7,23 @@
 // L diag(sqrt D) Z with numpy.  Here, per batch of B blocks of n x n (row-major,
 // block b at a + b n^2), all on the device with hand-written kernels:
 //
-//   * blocked right-looking Cholesky on 64 x 64 tiles, one launch per stage and
-//     panel k, every launch covering all B blocks (grid.y = batch):
-//       chol_diag    -- factor tile (k, k) in shared memory (unblocked, rank-1
-//                       updates) and invert it (row-wise substitution);
-//       chol_panel   -- panel tiles (I, k), I > k:  A_Ik <- A_Ik L_kk^-T as a
-//                       64 x 64 x 64 product with the inverse (the TRSM-by-
-//                       inverse of GPU LAPACKs), fused with the next
-//                       column's update inside a super-panel (chol_diag
-//                       solves tile k + 1 itself);
-//       chol_update  -- trailing tiles (I, J), k < J <= I:
-//                       A_IJ <- A_IJ - A_Ik A_Jk^T;
-//     the two products run on the FP64 tensor cores (mma.sync m8n8k4 f64,
-//     DMMA), 64 x 64 output tile per CTA, 4 warps of 32 x 32, operands staged
-//     in shared memory with a 68-double row pitch (conflict-free fragment
-//     loads);
+//   * blocked right-looking Cholesky on 64 x 64 tiles, every launch covering
+//     all B blocks:
+//       chol_diag    -- factor tile (k, k) in shared memory in 16-column
+//                       blocks (warp-register factor, per-row panel solve,
+//                       sub-block trailing update), the tile below riding
+//                       along as extra panel rows, and invert L_kk;
+//       chol_panel   -- panel tiles (I, k), I > k + 1:  A_Ik <- A_Ik L_kk^-T
+//                       as a 64 x 64 x 64 product with the inverse (the
+//                       TRSM-by-inverse of GPU LAPACKs), fused with the next
+//                       column's update inside a super-panel;
+//       chol_update  -- trailing tiles (I, J), J <= I, over a K range of
+//                       panel columns: A_IJ <- A_IJ - sum_k A_Ik A_Jk^T;
+//     the products run on the FP64 tensor cores (mma.sync m8n8k4 f64, DMMA;
+//     tcgen05 has no FP64 kind), 64 x 64 output tile per CTA, 4 warps of
+//     32 x 32, operands staged in shared memory at a padded pitch
+//     (conflict-free fragment loads); the schedule (super-panels, lazy
+//     per-column updates, look-ahead streams) is in sfb_chol_batch;
 //   * chol_finish    -- L = C / diag(C) below the diagonal, 1 on it, 0 above;
 //                       D = diag(C)^2 (grf.py:203-207);
 //   * lower_diag_mul -- out = L diag(s) Z, s = sqrt(D) or D: one warp per
