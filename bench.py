@@ -281,6 +281,7 @@ def run_normal(torch, sf, rank, world, steps, warmup, cfg, dtype):
 
 
 FISHER_WARM_S = 2.0  # steady-state warm-up of the Fisher workloads (seconds)
+FISHER_WARM_MAX_S = 120.0  # ... waiting at most this long for background memo builds
 
 def run_fisher(torch, sf, rank, world, steps, warmup, table, n, g, scratch):
     """One fisher_sim per step over this rank's item block + NCCL all-reduce."""
@@ -302,13 +303,22 @@ def run_fisher(torch, sf, rank, world, steps, warmup, table, n, g, scratch):
 
     for _ in range(warmup):
         step()
-    # then steady state: repeated calls on one table get the large memo set,
-    # built on a host thread after the second call (fisher.cu get_memo); keep
-    # stepping for FISHER_WARM_S so it has landed before the timed steps
-    t_end = time.perf_counter() + FISHER_WARM_S
-    while time.perf_counter() < t_end:
+    # then steady state: repeated calls on one table get the larger memo sets,
+    # built on host threads from the second call on (fisher.cu get_memo); keep
+    # stepping for FISHER_WARM_S and until no build is pending, so the final
+    # set has landed (and been uploaded) before the timed steps
+    from paper_2201_06604_b200 import _lib
+
+    t0 = time.perf_counter()
+    while True:
         step()
         torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if el >= FISHER_WARM_MAX_S or (el >= FISHER_WARM_S and
+                                       _lib.lib().sfb_fisher_memo_pending() == 0):
+            break
+    step()  # the first call on a newly installed set uploads it
+    torch.cuda.synchronize()
     barrier(torch, world)
     total_ms = 0.0
     for _ in range(steps):

@@ -191,6 +191,11 @@ int sfb_fisher_replicates_host(int64_t *h_cur, int64_t n_streams, const int64_t 
                                int64_t lf_len, double threshold, int64_t reps,
                                int64_t item_lo, int64_t item_hi, double *h_stats,
                                uint64_t *h_count, void *stream);
+/* Background memo builds in flight (sfb_fisher_replicates* upgrade a capped
+ * table's memo set on repeated use, on host threads; a call made while one is
+ * pending runs on the current set).  No reference counterpart: lets a caller
+ * that times steady-state calls wait until the set is final. */
+int sfb_fisher_memo_pending(void);
 /* _kernels.py:289-391 rcont2_table: one table from one 6-word state, run by
  * the same device sampler on one thread.  d_state: device int64[6] (mutated),
  * d_mat: device int64[nr*nc]. */

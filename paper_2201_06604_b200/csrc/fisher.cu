@@ -48,9 +48,15 @@ namespace sfb {
 // background -- 2^17 points, 2^26 words: T10 244 MB in ~0.7 s, T10 kernel
 // 23.8 -> 22.6 ms, month 5.88 -> 5.68 ms -- and the next call after it is
 // ready picks it up.  So a one-off call never waits for the large build and a
-// Monte Carlo loop over one table gets it after its first second.
+// Monte Carlo loop over one table gets it after its first second.  If level 1
+// is capped too, the same thread goes on to level 2 -- 2^20 points, 2^29
+// words (2 GB for T10, ~6 s on 16 host cores): T10 22.6 -> 21.7 ms per 16.8 M
+// tables, 1e9 C4-shaped tables 7.66e8 -> 8.09e8 /s (tools/fisher_time.py).
 constexpr int kDevMemoCellPtsLog2 = 17;
 constexpr int kDevMemoWordsLog2 = 26;
+constexpr int kDevMemo2CellPtsLog2 = 20;
+constexpr int kDevMemo2WordsLog2 = 29;
+static std::atomic<int> g_memo_pending{0};  // background builds in flight
 constexpr int64_t kMemoPrefetchMax = (int64_t)32 << 20;  // L2 prefetch at kernel start
 constexpr int kMaxChunks = 96;        // chunk jumps in the small parameter block
 constexpr int kMaxChunksLarge = 384;  // small grids (e.g. the default 64 x 16): 27 KB block
@@ -501,7 +507,7 @@ struct MemoEntry {
     std::shared_ptr<const HostMemo> memo;
     uint64_t version = 0, tick = 0;
     int level = 0;           // budget level of `memo` (see kDevMemoCellPtsLog2)
-    bool upgrading = false;  // a level-1 build is running
+    bool upgrading = false;  // a background build (level 1, then 2) is running
 };
 
 struct MemoCache {
@@ -515,8 +521,10 @@ static std::shared_ptr<HostMemo> build_memo(const std::vector<int64_t> &key, int
     std::vector<int32_t> rowm(key.begin(), key.begin() + nr);
     std::vector<int32_t> colm(key.begin() + nr + 1, key.begin() + nr + 1 + nc);
     auto hm = std::make_shared<HostMemo>();
-    const int pts = level ? tune_knob("SFB_MEMO_CELL_PTS_LOG2", kDevMemoCellPtsLog2) : 15;
-    const int words = level ? tune_knob("SFB_MEMO_WORDS_LOG2", kDevMemoWordsLog2) : 25;
+    const int pts = level == 2 ? tune_knob("SFB_MEMO2_CELL_PTS_LOG2", kDevMemo2CellPtsLog2)
+                    : level ? tune_knob("SFB_MEMO_CELL_PTS_LOG2", kDevMemoCellPtsLog2) : 15;
+    const int words = level == 2 ? tune_knob("SFB_MEMO2_WORDS_LOG2", kDevMemo2WordsLog2)
+                      : level ? tune_knob("SFB_MEMO_WORDS_LOG2", kDevMemoWordsLog2) : 25;
     build_memo_set(rowm.data(), nr, colm.data(), nc, ntot, LfPlain{lf}, kHostExpTab, *hm,
                    (size_t)1 << words, kMemoSigmas, tune_knob("SFB_FISHER_MEMO_INT", 1) != 0,
                    tune_knob("SFB_MEMO_RMAX_X10", 45) / 10.0, (size_t)1 << pts);
@@ -540,34 +548,51 @@ static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, co
     std::vector<int64_t> key(nrowt, nrowt + nr);
     key.push_back(-1);
     key.insert(key.end(), ncolt, ncolt + nc);
-    const int upgrade = tune_knob("SFB_FISHER_MEMO_UPGRADE", 1);  // 0 off, 2 synchronous
+    // 0 off, 1 background (levels 1 then 2), 2 / 3 synchronous level 1 / 2
+    const int upgrade = tune_knob("SFB_FISHER_MEMO_UPGRADE", 1);
+    const int max_level = std::min(2, std::max(1, tune_knob("SFB_FISHER_MEMO_LEVELS", 2)));
+    const int sync_level = upgrade == 2 ? 1 : upgrade == 3 ? 2 : 0;
     {
         std::lock_guard<std::mutex> g(mc.mu);
         MemoEntry *en = find_memo(mc, key, lf, lf_len);
-        if (en && !(upgrade == 2 && en->level == 0)) {
+        if (en && en->level >= sync_level) {
             en->tick = ++mc.tick;
             *version = en->version;
-            if (upgrade == 1 && en->level == 0 && en->memo->capped && !en->upgrading) {
-                // second use of a capped table: the large set in the background
+            if (upgrade == 1 && en->level < max_level && en->memo->capped && !en->upgrading) {
+                // repeated use of a capped table: the larger sets in the
+                // background, each installed (a new version: input caches
+                // re-upload) as soon as it is built
                 en->upgrading = true;
+                g_memo_pending.fetch_add(1);
                 std::vector<double> lfv(lf, lf + lf_len);
-                std::thread([key, lfv, nr, nc, ntot] {
-                    std::shared_ptr<HostMemo> big = build_memo(key, nr, nc, ntot, lfv.data(), 1);
-                    std::lock_guard<std::mutex> g2(mc.mu);
-                    MemoEntry *cur = find_memo(mc, key, lfv.data(), (int64_t)lfv.size());
-                    if (cur && cur->level == 0) {
-                        cur->memo = big;
-                        cur->level = 1;
-                        cur->version = ++mc.version;  // input caches re-upload
+                const int from = en->level;
+                std::thread([key, lfv, nr, nc, ntot, from, max_level] {
+                    for (int lvl = from + 1; lvl <= max_level; ++lvl) {
+                        std::shared_ptr<HostMemo> big =
+                            build_memo(key, nr, nc, ntot, lfv.data(), lvl);
+                        std::lock_guard<std::mutex> g2(mc.mu);
+                        MemoEntry *cur = find_memo(mc, key, lfv.data(), (int64_t)lfv.size());
+                        if (!cur) break;  // evicted meanwhile
+                        if (cur->level < lvl) {
+                            cur->memo = big;
+                            cur->level = lvl;
+                            cur->version = ++mc.version;
+                        }
+                        if (!big->capped) break;
                     }
-                    if (cur) cur->upgrading = false;
+                    {
+                        std::lock_guard<std::mutex> g2(mc.mu);
+                        MemoEntry *cur = find_memo(mc, key, lfv.data(), (int64_t)lfv.size());
+                        if (cur) cur->upgrading = false;
+                    }
+                    g_memo_pending.fetch_sub(1);
                 }).detach();
             }
             return en->memo;
         }
     }
     // build outside the lock (other tables' calls proceed meanwhile)
-    const int level = upgrade == 2 ? 1 : 0;
+    const int level = sync_level;
     std::shared_ptr<HostMemo> hm = build_memo(key, nr, nc, ntot, lf, level);
     std::lock_guard<std::mutex> g(mc.mu);
     // the same table built meanwhile (or a level-0 entry being replaced): reuse its slot
@@ -925,6 +950,8 @@ static int fisher_replicates_impl(int64_t *d_cur, int64_t n_streams, const int64
 }
 
 extern "C" {
+
+int sfb_fisher_memo_pending(void) { return g_memo_pending.load(); }
 
 // Host-buffer form of sfb_fisher_replicates: the call a host-authoritative
 // fisher_sim makes (fisher.py:147-157 with states, count and statistics in

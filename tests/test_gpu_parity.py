@@ -986,11 +986,12 @@ def test_fisher_host_and_device_states_agree(G, table_key, n, g):
         assert np.array_equal(a.current[w], orc.skip(seeds[w], reps * f)), w
 
 
-def test_fisher_large_memo_level_bit_exact(G, A, monkeypatch):
-    """The large memo set (SFB_FISHER_MEMO_UPGRADE=2: built synchronously at
-    the first use, with the budgets the background upgrade uses) gives the
-    golden counts, statistics and states bit for bit."""
-    monkeypatch.setenv("SFB_FISHER_MEMO_UPGRADE", "2")
+@pytest.mark.parametrize("level", [2, 3])
+def test_fisher_large_memo_level_bit_exact(G, A, monkeypatch, level):
+    """The large memo sets (SFB_FISHER_MEMO_UPGRADE=2 / 3: level 1 / 2 built
+    synchronously at the first use, with the budgets the background upgrade
+    uses) give the golden counts, statistics and states bit for bit."""
+    monkeypatch.setenv("SFB_FISHER_MEMO_UPGRADE", str(level))
     tabs = _tables(G, A)
     for key in ("F_T10_1e6", "F_month_s", "F_Ebig"):
         g = G[key]
@@ -1001,3 +1002,39 @@ def test_fisher_large_memo_level_bit_exact(G, A, monkeypatch):
         assert sha(st.current) == g["states_sha"]
         if want:
             assert np.array_equal(r.statistics, A[key + "_stats"])
+
+
+def test_fisher_background_memo_upgrades_land_and_agree(G):
+    """Repeated calls on a capped table start the background builds (level 1,
+    then 2); sfb_fisher_memo_pending() drops to 0 once both are installed, and
+    the results before, during and after the upgrades equal the first call's
+    (every memo level is bit-exact).  A T10 variant keeps the table's memo
+    fresh in this process."""
+    import time
+
+    from paper_2201_06604_b200 import _lib
+
+    t10 = np.array(G["T10"])
+    t10[0, 0] += 1
+    g = sf.WorkGrid(64, 32)
+    ref = None
+    t0 = time.perf_counter()
+    seen_pending = False
+    calls = 0
+    while time.perf_counter() - t0 < 120:
+        st = fresh(g.size)
+        r = sf.fisher_sim(t10, 20000, st, grid=g, return_stats=True)
+        calls += 1
+        if ref is None:
+            ref = (r.counts, r.statistics.copy(), st.current.copy())
+        else:
+            assert r.counts == ref[0]
+            assert np.array_equal(r.statistics, ref[1])
+            assert np.array_equal(st.current, ref[2])
+        pend = _lib.lib().sfb_fisher_memo_pending()
+        seen_pending |= pend > 0
+        if calls > 2 and pend == 0 and seen_pending:
+            break
+        time.sleep(0.05)
+    assert seen_pending, "no background memo build started"
+    assert _lib.lib().sfb_fisher_memo_pending() == 0

@@ -503,13 +503,14 @@ def test_device_fisher_sampler_on_host_matches_oracle(G, A, name):
     assert np.array_equal(st, rst)
 
 
-def test_device_fisher_sampler_large_memo_budget(G, monkeypatch):
-    """The level-1 (background-upgrade) memo budgets of the device path --
-    2^17 points per interior box, 2^26 record words -- on T10 (boxes for the
-    large interior cells, long truncated records): the sampler run on the host
-    == oracle, bit for bit."""
-    monkeypatch.setenv("SFB_MEMO_CELL_PTS_LOG2", "17")
-    monkeypatch.setenv("SFB_MEMO_WORDS_LOG2", "26")
+@pytest.mark.parametrize("pts,words", [(17, 26), (20, 29)])
+def test_device_fisher_sampler_large_memo_budget(G, monkeypatch, pts, words):
+    """The background-upgrade memo budgets of the device path -- level 1:
+    2^17 points per interior box, 2^26 record words; level 2: 2^20 / 2^29 --
+    on T10 (boxes for the large interior cells, long truncated records): the
+    sampler run on the host == oracle, bit for bit."""
+    monkeypatch.setenv("SFB_MEMO_CELL_PTS_LOG2", str(pts))
+    monkeypatch.setenv("SFB_MEMO_WORDS_LOG2", str(words))
     cnt, rcnt, cur, ref, st, rst = _host_fisher(G["T10"], 0, 32, reps_override=40, stats=True)
     assert cnt == rcnt
     assert np.array_equal(cur, ref)

@@ -49,6 +49,7 @@ for name, table, n, g, reps in [c for c in [("T4", T4, 10**6, (256, 64), 60),
                                 ("T4n256k", T4, 262144, (256, 64), 60),
                                 ("T4x4", T4, 4 * 10**6, (256, 64), 20),
                                 ("T10", G["T10"], (1 << 21) * 8, (2048, 1024), 8),
+                                ("T10c4", G["T10"], (1 << 21) * 477, (2048, 1024), 3),
                                 ("month", A["month"], 10**6, (256, 64), 10),
                                 ("week", A["week"], 10**6, (256, 64), 10)] if c[0] in CASES]:
     k, v = case(name, table, n, g, reps); out[k] = v
