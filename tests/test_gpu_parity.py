@@ -12,6 +12,7 @@ Bars:
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -1038,3 +1039,30 @@ def test_fisher_background_memo_upgrades_land_and_agree(G):
         time.sleep(0.05)
     assert seen_pending, "no background memo build started"
     assert _lib.lib().sfb_fisher_memo_pending() == 0
+
+
+def test_process_exits_cleanly_with_a_memo_build_in_flight(G, tmp_path):
+    """A process that leaves a background memo build running (detached host
+    thread) still exits with status 0: the memo cache is never destroyed, so
+    the thread cannot touch freed state during static destruction."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "exit_check.py"
+    script.write_text(
+        "import json, sys\n"
+        "import numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_2201_06604_b200 as sf\n"
+        "from paper_2201_06604_b200 import _lib\n"
+        f"t10 = np.array(json.load(open({os.path.join(root, 'tests', 'golden', 'golden.json')!r}))['T10'])\n"
+        "t10[1, 1] += 2\n"
+        "g = sf.WorkGrid(64, 32)\n"
+        "for i in range(3):\n"
+        "    st = sf.create_streams(sf.set_base_creator(), g.size)[0]\n"
+        "    sf.fisher_sim(t10, 20000, st, grid=g)\n"
+        "print('pending', _lib.lib().sfb_fisher_memo_pending())\n")
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "pending" in r.stdout
