@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag(double *a, int64_t n, 
     __shared__ long long dclk[24];
 #endif
     DCLK(0);
+    // launched with programmatic stream serialisation: everything below reads
+    // what the previous chain kernel wrote
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int b = blockIdx.y;
     if (info[b]) return;
     double *blk = a + (int64_t)b * n * n;
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(kGemmThreads) chol_panel(double *a, int64_t n,
     __shared__ long long dclk[8];
 #endif
     DCLK(0);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // see chol_diag
     const int b = blockIdx.y;
     if (info[b]) return;
     double *blk = a + (int64_t)b * n * n;
@@ -787,6 +791,25 @@ static void release(Scratch &sc, cudaStream_t st) {
     sc.used = true;
 }
 
+// chain kernels are launched with programmatic stream serialisation (PDL):
+// the next one is scheduled while the previous one's CTAs drain and waits in
+// griddepcontrol.wait, hiding the launch gap of the serial chain
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                cudaStream_t st, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 struct LookAhead {
     std::mutex mu;
     cudaStream_t sb = nullptr, sh = nullptr;  // bulk update (low priority), chain (high)
@@ -928,6 +951,7 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
     // i + 2 first (what the next "a" update waits for), then the rest, which
     // keeps running beside super-panel i + 1's chain.
     const bool split_b = tune_knob("SFB_CHOL_SPLIT_B", 1) != 0;
+    const bool pdl = tune_knob("SFB_CHOL_PDL", 1) != 0;
     const cudaStream_t caller = st;
     cudaEventRecord(la.ev_s, caller);  // the copy into d_lmat, the info reset, linv
     cudaStreamWaitEvent(la.sh, la.ev_s, 0);
@@ -941,8 +965,8 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
         // column's own update touches the tiles it updated)
         bool pending_r = false;
         for (int k = p0; k < p1; ++k) {
-            chol_diag<<<dim3(1, (unsigned)batch), kDiagThreads, kDiagSmem, st>>>(
-                d_lmat, n, k, info, linv, k + 1 < nt);
+            launch_chain(chol_diag, dim3(1, (unsigned)batch), dim3(kDiagThreads), kDiagSmem, st,
+                         pdl, d_lmat, n, k, info, linv, (int)(k + 1 < nt));
             if (k + 1 >= nt) continue;
             if (k + 1 < p1) {
                 // the next column's update also writes tiles the previous
@@ -950,8 +974,9 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                 // column update on sc) wrote
                 if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);
                 if (col_pending) cudaStreamWaitEvent(st, la.ev_col[k + 1 - p0], 0);
-                chol_panel<true><<<dim3((unsigned)(nt - k - 1), (unsigned)batch), kGemmThreads,
-                                   kPanelSmem, st>>>(d_lmat, n, k, info, linv);
+                launch_chain(chol_panel<true>, dim3((unsigned)(nt - k - 1), (unsigned)batch),
+                             dim3(kGemmThreads), kPanelSmem, st, pdl, d_lmat, n, k,
+                             (const int *)info, (const double *)linv);
                 pending_r = false;
                 if (k + 2 < p1) {
                     // column k + 2 gets the contributions of columns p0 .. k
@@ -979,8 +1004,9 @@ int sfb_chol_batch(const double *d_a, int64_t n, int64_t batch, double *d_lmat, 
                     }
                 }
             } else if (k + 2 < nt) {
-                chol_panel<false><<<dim3((unsigned)(nt - k - 2), (unsigned)batch), kGemmThreads,
-                                    kPanelSmem, st>>>(d_lmat, n, k, info, linv);
+                launch_chain(chol_panel<false>, dim3((unsigned)(nt - k - 2), (unsigned)batch),
+                             dim3(kGemmThreads), kPanelSmem, st, pdl, d_lmat, n, k,
+                             (const int *)info, (const double *)linv);
             }
         }
         if (pending_r) cudaStreamWaitEvent(st, la.ev_r, 0);
