@@ -57,6 +57,13 @@ constexpr int kDevMemoWordsLog2 = 26;
 constexpr int kDevMemo2CellPtsLog2 = 20;
 constexpr int kDevMemo2WordsLog2 = 29;
 static std::atomic<int> g_memo_pending{0};  // background builds in flight
+// background builds run one at a time (each is multi-threaded and a level-2
+// set holds up to 2 GB while it is built): many capped tables used in a row
+// queue up instead of oversubscribing the host
+static std::mutex &build_mutex() {
+    static std::mutex &m = *new std::mutex;
+    return m;
+}
 constexpr int64_t kMemoPrefetchMax = (int64_t)32 << 20;  // L2 prefetch at kernel start
 constexpr int kMaxChunks = 96;        // chunk jumps in the small parameter block
 constexpr int kMaxChunksLarge = 384;  // small grids (e.g. the default 64 x 16): 27 KB block
@@ -568,8 +575,15 @@ static std::shared_ptr<const HostMemo> get_memo(const int64_t *nrowt, int nr, co
                 const int from = en->level;
                 std::thread([key, lfv, nr, nc, ntot, from, max_level] {
                     for (int lvl = from + 1; lvl <= max_level; ++lvl) {
-                        std::shared_ptr<HostMemo> big =
-                            build_memo(key, nr, nc, ntot, lfv.data(), lvl);
+                        std::shared_ptr<HostMemo> big;
+                        {
+                            std::lock_guard<std::mutex> gb(build_mutex());
+                            {  // evicted while queued: nothing to build for
+                                std::lock_guard<std::mutex> g2(mc.mu);
+                                if (!find_memo(mc, key, lfv.data(), (int64_t)lfv.size())) break;
+                            }
+                            big = build_memo(key, nr, nc, ntot, lfv.data(), lvl);
+                        }
                         std::lock_guard<std::mutex> g2(mc.mu);
                         MemoEntry *cur = find_memo(mc, key, lfv.data(), (int64_t)lfv.size());
                         if (!cur) break;  // evicted meanwhile
