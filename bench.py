@@ -381,6 +381,27 @@ GRF_BATCH = [(1.0, 8.0, 1.0, 1.0, 0.0), (1.5, 12.0, 2.0, 2.0, 0.5), (0.5, 6.0, 1
              (2.0, 10.0, 1.0, 1.5, 1.0)]
 
 
+def time_chol(torch, sf):
+    """Device time (ms, best of 3, CUDA events) of one sfb_chol_batch call on
+    the GRF acceptance batch (4 x 5130^2)."""
+    try:
+        cov = sf.matern_cov([sf.MaternParams(*p) for p in GRF_BATCH], sf.GridSpec(90, 57, 1.0))
+        sf.chol_batch(cov)  # warm-up
+        best = None
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s.record()
+            sf.chol_batch(cov)
+            e.record()
+            e.synchronize()
+            ms = s.elapsed_time(e)
+            best = ms if best is None else min(best, ms)
+        return best
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def run_grf(api, steps):
     """simulate_grf on the reference's acceptance-11 batch
     (four Matern parameter sets on a 90 x 57 grid -> four 5130 x 5130
@@ -684,6 +705,16 @@ def run_probes(torch, _lib):
         ms = tm.stop()
         best = ms if best is None else min(best, ms)
     out["fp64_ops_per_s"] = blocks * 256 * iters * 8 / (best / 1e3)  # DFMA/s (1 op each)
+    # FP64 tensor cores: 4 warps x 4 CTAs per SM, 16 independent DMMA chains each
+    blocks, iters = 148 * 4, 2048
+    _lib.check(_lib.lib().sfb_probe_dmma(_lib.dptr(d), blocks, iters, st))
+    best = None
+    for _ in range(3):
+        tm.start()
+        _lib.check(_lib.lib().sfb_probe_dmma(_lib.dptr(d), blocks, iters, st))
+        ms = tm.stop()
+        best = ms if best is None else min(best, ms)
+    out["dmma_flops_per_s"] = blocks * 4 * iters * 16 * 512 / (best / 1e3)
     return out
 
 
@@ -818,6 +849,17 @@ def main():
                                        config="SURVEY 8(f) item 4: simulate_grf, 4 Matern sets "
                                               "on a 90x57 grid (4 x 5130^2 LDL^T), 2 "
                                               "realisations, host fields out (best of 3)")
+        chol_ms = time_chol(torch, sf)
+        if probe and chol_ms:
+            ach = 4 * 5130 ** 3 / 3 / (chol_ms / 1e3)
+            workloads["grf_4x5130"]["roofline"] = {
+                "bound": "tensor", "kernel": "sfb_chol_batch (chol_update / chol_panel DMMA "
+                "tile products, chol_diag chain)", "achieved": ach / 1e12,
+                "peak": probe["dmma_flops_per_s"] / 1e12, "unit": "TFLOP/s",
+                "frac": ach / probe["dmma_flops_per_s"], "chol_ms": chol_ms,
+                "note": "n^3/3 flops per 5130^2 block x 4 over the device time of one "
+                        "sfb_chol_batch call (CUDA events, best of 3); peak = sfb_probe_dmma "
+                        "(mma.sync.m8n8k4.f64 issue rate; tcgen05 has no FP64 kind)"}
     e2e = run_uniform_e2e(torch, sf, rank, world, min(args.steps, 3), C5)
     if args.only in (None, "fisher") and world == 1:
         fe = run_fisher_e2e(torch, sf, 3, T4, 10 ** 6, (256, 64))

@@ -209,6 +209,10 @@ int sfb_rcont2_table(const int64_t *nrowt, int nr, const int64_t *ncolt, int nc,
 int sfb_probe_rsqrt(const double *d_x, double *d_y, int64_t n, void *stream);
 /* FP64-pipe roofline probe (bench.py): blocks x 256 threads x iters x 8 DFMA */
 int sfb_probe_fp64(double *d_out, int64_t blocks, int iters, void *stream);
+/* FP64 tensor-core (DMMA) probe: `blocks` CTAs of 4 warps, each warp `iters`
+ * x 16 independent mma.sync.m8n8k4.f64 (512 flops each); bench.py derives the
+ * DMMA roofline denominator of the GRF Cholesky from its time. */
+int sfb_probe_dmma(double *d_out, int64_t blocks, int iters, void *stream);
 /* write-only HBM probe: fills `bytes` (multiple of 16) with 16-byte stores;
  * variant 0 = grid-stride sweep, 1 = per-CTA contiguous segments (fill shape),
  * 2 = per-CTA segments with 32-byte stores */

@@ -58,6 +58,7 @@ _SIGS = {
     "sfb_rcont2_table": ([_i64p, _int, _i64p, _int, _f64p, _i64, _vp, _vp, _vp], _int),
     "sfb_fisher_memo_pending": ([], _int),
     "sfb_probe_fp64": ([_vp, _i64, _int, _vp], _int),
+    "sfb_probe_dmma": ([_vp, _i64, _int, _vp], _int),
     "sfb_probe_rsqrt": ([_vp, _vp, _i64, _vp], _int),
     "sfb_bessel_k": ([ctypes.c_double, _vp, _i64, _vp, _vp], _int),
     "sfb_matern_correlation": ([ctypes.c_double, ctypes.c_double, _vp, _i64, _vp, _vp], _int),

@@ -93,9 +93,37 @@ __global__ void __launch_bounds__(256) write_probe_bulk_kernel(unsigned char *ou
     }
 }
 
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) issue rate: every warp runs
+// 16 independent accumulators (the shape of the Cholesky tile products) on
+// register operands; 512 flops per instruction
+__global__ void __launch_bounds__(128) dmma_probe_kernel(double *out, int iters, double a0) {
+    double acc[16][2];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q][0] = acc[q][1] = 0.0;
+    double a = a0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[q][0]), "+d"(acc[q][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s += acc[q][0] + acc[q][1];
+    if (s == 12345.678) out[0] = s;  // keeps the chains live
+}
+
 }  // namespace sfb
 
 using namespace sfb;
+
+extern "C" int sfb_probe_dmma(double *d_out, int64_t blocks, int iters, void *stream) {
+    dmma_probe_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(d_out, iters, 1e-3);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SFB_E_CUDA, "dmma probe: %s", cudaGetErrorString(e));
+    return SFB_OK;
+}
 
 extern "C" int sfb_probe_write(void *d_out, int64_t bytes, int variant, void *stream) {
     const int64_t n = bytes / 16;
