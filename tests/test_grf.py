@@ -220,6 +220,25 @@ def test_chol_batch_schedules_agree(monkeypatch, panel, split):
 
 
 @pytest.mark.gpu
+def test_chol_batch_default_schedule_with_bulk_updates():
+    """n = 1500 (24 tiles, three 8-tile super-panels) on the default
+    schedule: the per-column look-ahead updates on their own stream and the
+    bulk update split into near / far columns all run; L and D match the
+    oracle (LAPACK)."""
+    n, nb = 1500, 2
+    rng = np.random.default_rng(1500)
+    blocks = []
+    for _ in range(nb):
+        a = rng.standard_normal((n, n))
+        blocks.append(a @ a.T + n * np.eye(n))
+    data = np.vstack(blocks)
+    lmat, diag = sf.chol_batch(BatchedMatrix(data, nb))
+    rl, rd = og.chol_batch(data, nb)
+    assert np.allclose(lmat.data, rl, rtol=1e-10, atol=1e-12)
+    assert np.allclose(diag.data, rd, rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.gpu
 def test_chol_batch_concurrent_threads_and_streams():
     """Two host threads factor different batches on their own CUDA streams at
     once (the per-device look-ahead streams, events and scratch are shared
