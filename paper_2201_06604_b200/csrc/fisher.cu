@@ -208,14 +208,17 @@ __global__ void __launch_bounds__(kFisherThreads, MINB) fisher_kernel(const Fish
                                              ((const unsigned char *)a.memo.box - blob));
         }
         __syncthreads();
-        if (gtid < a.nunits) {  // one unit per thread
-            int *jw = (int *)(smem + off_jw) + threadIdx.x;
+        // one unit per thread, or (SFB_FISHER_UPT > 1) a few grid-stride
+        // units per thread so the CTA setup above is amortised
+        const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+        int *jw = (int *)(smem + off_jw) + threadIdx.x;
+        for (int64_t u = gtid; u < a.nunits; u += gstride) {
             if (LF_SMEM)
-                hits = run_unit<WALK, NR, NC, (NR == 0)>(a, jumps, gtid, srow, scol, LfShared{lfs}, exptab, jw,
-                                      (int)blockDim.x, memo);
+                hits += run_unit<WALK, NR, NC, (NR == 0)>(a, jumps, u, srow, scol, LfShared{lfs}, exptab, jw,
+                                       (int)blockDim.x, memo);
             else
-                hits = run_unit<WALK, NR, NC, (NR == 0)>(a, jumps, gtid, srow, scol, LfGlobal{a.lf}, exptab, jw,
-                                      (int)blockDim.x, memo);
+                hits += run_unit<WALK, NR, NC, (NR == 0)>(a, jumps, u, srow, scol, LfGlobal{a.lf}, exptab, jw,
+                                       (int)blockDim.x, memo);
         }
     }
     // warp shuffle -> shared -> one atomic per CTA, all in 64 bits
@@ -864,7 +867,8 @@ static int fisher_replicates_impl(int64_t *d_cur, int64_t n_streams, const int64
     };
     const bool lf_smem = layout(true) <= 110 * 1024;
     size_t smem = layout(lf_smem);
-    unsigned blocks = (unsigned)ceil_div(a.nunits, kFisherThreads);
+    const int upt = std::max(1, tune_knob("SFB_FISHER_UPT", 1));
+    unsigned blocks = (unsigned)ceil_div(ceil_div(a.nunits, upt), kFisherThreads);
     a.jwork_global = nullptr;
     a.jstride = 0;
     const bool wide = smem > (size_t)kMaxFisherSmem;
