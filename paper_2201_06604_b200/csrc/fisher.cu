@@ -49,13 +49,14 @@ namespace sfb {
 // 23.8 -> 22.6 ms, month 5.88 -> 5.68 ms -- and the next call after it is
 // ready picks it up.  So a one-off call never waits for the large build and a
 // Monte Carlo loop over one table gets it after its first second.  If level 1
-// is capped too, the same thread goes on to level 2 -- 2^20 points, 2^29
-// words (2 GB for T10, ~6 s on 16 host cores): T10 22.6 -> 21.7 ms per 16.8 M
-// tables, 1e9 C4-shaped tables 7.66e8 -> 8.09e8 /s (tools/fisher_time.py).
+// is capped too, the same thread goes on to level 2 -- 2^21 points, 2^30
+// words (4 GB for T10, ~12 s on 16 host cores): T10 22.6 -> 20.9 ms per
+// 16.8 M tables (2^20 / 2^29: 21.3 ms), 1e9 C4-shaped tables 1208 -> 1188 ms
+// against 2^20 / 2^29 (tools/fisher_time.py).
 constexpr int kDevMemoCellPtsLog2 = 17;
 constexpr int kDevMemoWordsLog2 = 26;
-constexpr int kDevMemo2CellPtsLog2 = 20;
-constexpr int kDevMemo2WordsLog2 = 29;
+constexpr int kDevMemo2CellPtsLog2 = 21;
+constexpr int kDevMemo2WordsLog2 = 30;
 static std::atomic<int> g_memo_pending{0};  // background builds in flight
 // background builds run one at a time (each is multi-threaded and a level-2
 // set holds up to 2 GB while it is built): many capped tables used in a row
