@@ -59,7 +59,7 @@ constexpr int kDevMemo2CellPtsLog2 = 21;
 constexpr int kDevMemo2WordsLog2 = 30;
 static std::atomic<int> g_memo_pending{0};  // background builds in flight
 // background builds run one at a time (each is multi-threaded and a level-2
-// set holds up to 2 GB while it is built): many capped tables used in a row
+// set holds up to 4 GB while it is built): many capped tables used in a row
 // queue up instead of oversubscribing the host
 static std::mutex &build_mutex() {
     static std::mutex &m = *new std::mutex;

@@ -503,10 +503,10 @@ def test_device_fisher_sampler_on_host_matches_oracle(G, A, name):
     assert np.array_equal(st, rst)
 
 
-@pytest.mark.parametrize("pts,words", [(17, 26), (20, 29)])
+@pytest.mark.parametrize("pts,words", [(17, 26), (21, 30)])
 def test_device_fisher_sampler_large_memo_budget(G, monkeypatch, pts, words):
     """The background-upgrade memo budgets of the device path -- level 1:
-    2^17 points per interior box, 2^26 record words; level 2: 2^20 / 2^29 --
+    2^17 points per interior box, 2^26 record words; level 2: 2^21 / 2^30 --
     on T10 (boxes for the large interior cells, long truncated records): the
     sampler run on the host == oracle, bit for bit."""
     monkeypatch.setenv("SFB_MEMO_CELL_PTS_LOG2", str(pts))
